@@ -1,0 +1,236 @@
+/*
+ * b200ring.h — C ABI of the B200-native double-ring tensor transport.
+ *
+ * Implements the hot path of arXiv 2601.20655 §6 "RDMA Network" / §6.1 "Ring
+ * Buffer": a multi-producer / single-consumer ring of
+ * variable-size messages held in the consumer's memory, written one-sidedly by
+ * producers, with a size region whose busy bits only the consumer clears.
+ * On one 8xB200 box the one-sided RDMA verbs become SM-issued
+ * NVLink 5 peer stores and system-scope atomics into a ring in the consumer
+ * GPU's HBM.  Readings of the paper are cited as R<n>.
+ *
+ * Conventions for every entry point
+ *   - Plain C types only; device pointers are `void*` / `uint64_t`; CUDA streams
+ *     are passed as `void*` (a cudaStream_t; NULL = the legacy default stream).
+ *   - Synchronous errors (bad arguments, CUDA/IPC failures) are the return
+ *     value.  Data-path outcomes (RING_FULL, RING_EMPTY, RING_ETIMEDOUT,
+ *     RING_ECORRUPT, RING_EMSGSIZE on copy-out) are written by the kernels to
+ *     device status words / view records in stream order: no host
+ *     synchronisation happens on the data path ("no CPU
+ *     intervention").
+ *   - Every device-side spin (lock, credit, new data) is bounded by the
+ *     timeout set with ring_set_timeout_ns (default 2 s) and then reports
+ *     RING_ETIMEDOUT instead of hanging (R12).
+ *   - Not thread-safe per handle: one host thread / one stream per ring_t
+ *     (the single consumer) and per ring_peer_t (one
+ *     producer stream).
+ */
+#ifndef B200RING_H
+#define B200RING_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RING_OK = 0,
+  RING_EINVAL = 1,     /* bad argument (zero sizes, N not a power of two, R not a multiple of 128, ...) */
+  RING_ENOMEM = 2,     /* device allocation failed */
+  RING_EMSGSIZE = 3,   /* entry footprint align_up(64+len,128) > R (R15), or copy-out buffer too small */
+  RING_FULL = 4,       /* RING_TRY put found insufficient space: "release the lock and abort" */
+  RING_EMPTY = 5,      /* RING_TRY get found no new data */
+  RING_ETIMEDOUT = 6,  /* a device spin exceeded its budget */
+  RING_ECORRUPT = 7,   /* header checksum mismatch: entry discarded and consumed */
+  RING_ECUDA = 8,      /* a CUDA runtime call failed (see ring_last_cuda_error) */
+  RING_EPEER = 9,      /* no peer access between the two devices / IPC open failed */
+  RING_EPENDING = 10   /* initial value of a device status word not yet written */
+} ring_status_t;
+
+/* flags for ring_put* / ring_get* */
+#define RING_BLOCK 0u        /* wait for credit / data (default, R12) */
+#define RING_TRY 1u          /* do not wait: RING_FULL / RING_EMPTY */
+#define RING_NO_TIMESTAMP 2u /* leave t_put / t_visible zero */
+
+/* flags for ring_create */
+#define RING_CREATE_DEFAULT 0u
+#define RING_CREATE_LOCAL 1u /* every producer runs on the ring's own device: gpu-scope ordering (cheaper fences) */
+
+/* Geometry limits (R5, R8) */
+#define RING_ENTRY_ALIGN 128u
+#define RING_HDR_BYTES 64u
+#define RING_MAX_SLOTS (1u << 23)
+#define RING_MAX_PRODUCERS 64u
+
+typedef struct ring_s* ring_t;           /* consumer side; OWNS the ring allocation in HBM */
+typedef struct ring_peer_s* ring_peer_t; /* producer side; BORROWS a mapping of the ring, OWNS its local state */
+typedef struct router_s* router_t;       /* stage router (NodeManager / ResultDeliver stand-in) */
+
+/* Opaque, position-independent handle exchanged between processes (e.g. with a
+ * torch.distributed all_gather of 128-byte tensors).  Carries a CUDA IPC memory
+ * handle plus the ring geometry. */
+typedef struct { unsigned char bytes[128]; } ring_handle_t;
+
+/* User-supplied header fields of a workflow message (UUID
+ * assigned by the proxy, proxy timestamp, application ID, stage). 32 bytes. */
+typedef struct {
+  uint8_t uid[16];
+  uint64_t accepted_at;
+  uint32_t app_id;
+  uint16_t stage;
+  uint16_t reserved; /* must be 0 */
+} ring_hdr_t;
+
+/* One message of a put batch, in DEVICE memory of the producer GPU. 48 bytes. */
+typedef struct {
+  uint64_t src;      /* device pointer to the payload (readable by the producer GPU) */
+  uint64_t len;      /* payload bytes (0 allowed, R19) */
+  ring_hdr_t hdr;
+} ring_msg_t;
+
+/* Result of one get, written by the get kernel to DEVICE memory. 128 bytes.
+ * `header` is the entry header exactly as read from the ring (64 bytes,
+ * layout R11: crc32[0,4) uid[4,20) accepted_at[20,28) app_id[28,32)
+ * stage[32,34) payload_len[34,38) reserved[38,44) producer_id[44,48)
+ * seq[48,52) epoch[52,54) flags[54,56) t_put[56,64)). */
+typedef struct {
+  uint64_t offset;     /* payload byte offset inside the buffer region (entry start + 64) */
+  uint64_t len;        /* payload bytes (from the header; 0 if corrupt) */
+  uint64_t footprint;  /* f from the size slot */
+  uint64_t start;      /* entry start offset inside the buffer region */
+  uint32_t slot_seq;   /* size-region sequence number (24 bit) */
+  uint32_t status;     /* RING_OK / RING_ECORRUPT / RING_EMPTY / RING_ETIMEDOUT / RING_EMSGSIZE */
+  uint64_t t_visible;  /* %globaltimer (ns) when the consumer saw the entry */
+  uint64_t reserved[2];
+  uint8_t header[64];
+} ring_view_t;
+
+/* Geometry / addresses of a ring (host-side query). */
+typedef struct {
+  int device;
+  uint32_t n_slots;        /* N */
+  uint32_t max_producers;
+  uint64_t data_bytes;     /* R */
+  uint64_t base;           /* device pointer of the ring allocation (consumer GPU) */
+  uint64_t data;           /* device pointer of the buffer region = base + data_offset */
+  uint64_t data_offset;
+  uint64_t alloc_bytes;
+} ring_info_t;
+
+/* ---- lifetime -------------------------------------------------------------
+ * ring_create: allocate and zero one ring on `device` (lock
+ * region, header with head/tail, buffer region of `data_bytes` = R bytes, size
+ * region of `n_slots` = N slots).  R must be a positive multiple of 128 below
+ * 2^40; N a power of two <= 2^23; 1 <= max_producers <= 64.  With
+ * max_producers == 1 the lock is elided (R14).  Layout: DESIGN.md §3. */
+ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uint32_t max_producers,
+                          uint32_t flags, ring_t* out);
+/* Free the ring.  All peers must be detached first (their mappings are borrowed). */
+ring_status_t ring_destroy(ring_t ring);
+ring_status_t ring_get_info(ring_t ring, ring_info_t* out);
+/* Export a handle for producers in other processes (CUDA IPC) or this process. */
+ring_status_t ring_export(ring_t ring, ring_handle_t* out);
+
+/* ring_attach_peer: map the ring of `h` for a producer running on
+ * `producer_device` with id `producer_id` (< max_producers, unique per ring).
+ * Same process: direct pointer + cudaDeviceEnablePeerAccess; other process:
+ * cudaIpcOpenMemHandle.  Allocates the producer-local state (head mirror,
+ * message counters) on `producer_device` and returns its handle in
+ * `mirror_out`, which the consumer passes to ring_bind_mirror so that releases
+ * push the head to this producer (credit ring, R1).  RING_EPEER if the devices
+ * cannot access each other. */
+ring_status_t ring_attach_peer(const ring_handle_t* h, int producer_device, uint32_t producer_id,
+                               ring_peer_t* out, ring_handle_t* mirror_out);
+/* Consumer side: register producer `producer_id`'s head mirror.  Until bound,
+ * that producer reads the head word over NVLink instead (correct, slower). */
+ring_status_t ring_bind_mirror(ring_t ring, uint32_t producer_id, const ring_handle_t* mirror);
+ring_status_t ring_detach(ring_peer_t peer);
+
+/* ---- producer ----------------------------------------------------------------
+ * ring_put_batch: append `n` messages (device array `d_msgs` on the producer
+ * GPU) in order, as the sender's 8 steps each: lock (MPSC
+ * only), read tail, GH stale-slot check, space check (PAD entry at the wrap,
+ * R3/R4), write the 64-B header + payload into the peer ring (WB), set the
+ * size slot busy|f (WL), advance the tail (UH, release at system scope),
+ * unlock.  One kernel launch; copies of message k+1 overlap the publish of k.
+ * `d_status` (device, n words) receives one ring_status_t per message
+ * (RING_OK / RING_FULL under RING_TRY / RING_ETIMEDOUT / RING_EMSGSIZE).
+ * The payloads must stay valid until the launch completes in stream order.
+ * Header seq (R18) = this attachment's running message count. */
+ring_status_t ring_put_batch(ring_peer_t peer, const ring_msg_t* d_msgs, uint32_t n, uint32_t flags,
+                             uint32_t* d_status, void* stream);
+/* Single message convenience form: `d_payload` device pointer, `hdr` host
+ * pointer (copied into the launch), one status word. */
+ring_status_t ring_put(ring_peer_t peer, const void* d_payload, uint64_t len, const ring_hdr_t* hdr,
+                       uint32_t flags, uint32_t* d_status, void* stream);
+/* Tuning: copy CTAs and threads per CTA of this attachment's put kernel
+ * (0 = default), copy engine (0 = 16-B vector LSU, 1 = TMA bulk). */
+ring_status_t ring_peer_config(ring_peer_t peer, uint32_t copy_ctas, uint32_t threads, uint32_t copy_mode);
+/* Host-side count of messages this attachment has submitted (= next header seq). */
+uint64_t ring_peer_submitted(ring_peer_t peer);
+
+/* ---- consumer ------------------------------------------------------------------
+ * ring_get: receive the next `n` entries (receiver steps 1-3, PAPER.md:711-715,
+ * plus the checksum check): poll the tail (R7), read the
+ * size slot (stepping over PAD entries, R3), read the header, verify the CRC,
+ * and write one view record per entry to `d_views` (device, n records).  If
+ * `d_dst` is not NULL the payload of entry i is also copied to
+ * d_dst + i*dst_stride (RING_EMSGSIZE in the view if len > dst_stride); else
+ * the view points into the ring (zero copy, valid until released).  Does not
+ * release.  RING_TRY: entries with nothing to read get status RING_EMPTY. */
+ring_status_t ring_get(ring_t ring, uint32_t n, ring_view_t* d_views, void* d_dst, uint64_t dst_stride,
+                       uint32_t flags, void* stream);
+/* ring_release: receiver steps 4-5 for the `count` oldest
+ * received entries, in order (R13): clear the busy bits, advance the head with
+ * the pointer formulas, free PAD slots already passed, then
+ * push the head to every bound producer mirror (credit).  `count` larger than
+ * the number held is clamped. */
+ring_status_t ring_release(ring_t ring, uint32_t count, void* stream);
+/* ring_consume: ring_get + ring_release of each entry as soon as it has been
+ * read (and copied, if d_dst != NULL): the paper's receiver loop as one launch. */
+ring_status_t ring_consume(ring_t ring, uint32_t n, ring_view_t* d_views, void* d_dst, uint64_t dst_stride,
+                           uint32_t flags, void* stream);
+/* Tuning: CTAs / threads of the copy-out get (0 = default). */
+ring_status_t ring_config(ring_t ring, uint32_t copy_ctas, uint32_t threads);
+
+/* ---- inspection (tests, debugging; synchronous) ---------------------------------
+ * Copy the control words and size slots to host memory: lock, tail, head,
+ * read cursor, and `n_slots` slot words (host array of N u64). */
+ring_status_t ring_read_image(ring_t ring, uint64_t* lock, uint64_t* tail, uint64_t* head, uint64_t* cursor,
+                              uint64_t* slots);
+/* Copy `len` bytes at `offset` of the buffer region to / from host memory
+ * (synchronous; tests: ring-image comparison and corruption injection). */
+ring_status_t ring_read_data(ring_t ring, uint64_t offset, uint64_t len, void* host_dst);
+ring_status_t ring_write_data(ring_t ring, uint64_t offset, uint64_t len, const void* host_src);
+
+/* ---- stage router (PAPER.md:524-532 round-robin ResultDeliver; PAPER.md:914-924
+ * NodeManager reassignment, mechanism only) ------------------------------------------
+ * A device-resident route table on the producer GPU: for each (app_id, stage)
+ * a list of up to 8 destination attachments, a round-robin counter and an epoch.
+ * router_set_route replaces the list and flips the epoch; puts already launched
+ * finish to their old destination. */
+ring_status_t router_create(int device, uint32_t max_routes, router_t* out);
+ring_status_t router_destroy(router_t r);
+ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, const ring_peer_t* dests, uint32_t n,
+                               void* stream);
+/* Routed put: each message of the batch picks dests[rr++ % n] of the route for
+ * its (hdr.app_id, hdr.stage), then runs the sender steps on that ring.
+ * The chosen destination index is written to d_dest (device, n words) if not NULL. */
+ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, uint32_t flags, uint32_t* d_status,
+                              uint32_t* d_dest, void* stream);
+
+/* ---- misc ------------------------------------------------------------------------ */
+ring_status_t ring_set_timeout_ns(uint64_t ns);
+const char* ring_strerror(ring_status_t s);
+const char* ring_last_cuda_error(void);
+/* Number of kernels this library has launched in this process (for bench accounting). */
+uint64_t ring_launch_count(void);
+/* Footprint of a payload: align_up(64 + len, 128) (R9, R11). */
+uint64_t ring_footprint(uint64_t len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200RING_H */

@@ -1,0 +1,663 @@
+// host.cu — the C ABI of include/b200ring.h: ring lifetime, IPC handles,
+// attachment of producers, launch configuration of the put / get / release
+// kernels and the stage router.  No protocol step runs here: the host only
+// validates arguments, allocates, maps and launches ("no CPU
+// intervention" on the data path).
+#include <unistd.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "ring_internal.h"
+
+using namespace b200ring;
+
+namespace {
+
+thread_local char g_cuda_err[512] = "";
+std::atomic<uint64_t> g_timeout_ns{2000000000ull};
+std::atomic<uint64_t> g_launches{0};
+std::mutex g_mu;
+const uint32_t g_token = 0x9e3779b9u ^ (uint32_t)getpid() ^ (uint32_t)((uintptr_t)&g_mu & 0xffffffffu);
+
+constexpr uint32_t kMagicRing = 0x52494e47;    // "RING"
+constexpr uint32_t kMagicMirror = 0x4d495252;  // "MIRR"
+
+struct HandleBlob {
+  uint32_t magic;
+  int32_t device;
+  int32_t pid;
+  uint32_t token;
+  uint64_t ptr;          // device pointer in the exporting process
+  uint64_t R;
+  uint32_t N;
+  uint32_t max_producers;
+  uint32_t flags;
+  uint32_t producer_id;  // mirror handles
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(HandleBlob) <= sizeof(ring_handle_t), "handle too large");
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      snprintf(g_cuda_err, sizeof g_cuda_err, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+               __FILE__, __LINE__);                                                          \
+      return RING_ECUDA;                                                                     \
+    }                                                                                        \
+  } while (0)
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---- CRC-32 position table (R10) -------------------------------------------
+// Built from this file's own bitwise CRC-32 (reflected 0xEDB88320): the
+// register contribution of each bit of the 52 CRC'd header bytes, laid out
+// [bit 0..31][header word 1..13], followed by crc32(52 zero bytes).
+uint32_t crc_register(const uint8_t* p, size_t n, uint32_t reg) {
+  for (size_t i = 0; i < n; ++i) {
+    reg ^= p[i];
+    for (int b = 0; b < 8; ++b) reg = (reg & 1) ? (reg >> 1) ^ 0xEDB88320u : reg >> 1;
+  }
+  return reg;
+}
+std::vector<uint32_t> build_crc_table() {
+  std::vector<uint32_t> t(kCrcTableWords);
+  uint8_t msg[52];
+  for (int w = 0; w < kCrcWords; ++w)
+    for (int b = 0; b < 32; ++b) {
+      memset(msg, 0, sizeof msg);
+      msg[4 * w + b / 8] = (uint8_t)(1u << (b % 8));
+      t[b * kCrcWords + w] = crc_register(msg, 52, 0u);
+    }
+  memset(msg, 0, sizeof msg);
+  t[32 * kCrcWords] = crc_register(msg, 52, 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+  return t;
+}
+uint32_t* g_crc_dev[64] = {};
+ring_status_t crc_table_dev(int device, const uint32_t** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (device < 0 || device >= 64) return RING_EINVAL;
+  if (!g_crc_dev[device]) {
+    DevGuard g(device);
+    static const std::vector<uint32_t> host = build_crc_table();
+    uint32_t* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, host.size() * 4));
+    CUDA_TRY(cudaMemcpy(d, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
+    g_crc_dev[device] = d;
+  }
+  *out = g_crc_dev[device];
+  return RING_OK;
+}
+
+ring_status_t enable_peer(int from, int to) {
+  if (from == to) return RING_OK;
+  int can = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can, from, to));
+  if (!can) return RING_EPEER;
+  DevGuard g(from);
+  cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return RING_OK;
+  }
+  CUDA_TRY(e);
+  return RING_OK;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct ring_s {
+  int device = 0;
+  uint8_t* base = nullptr;
+  uint64_t R = 0, data_off = 0, alloc = 0;
+  uint32_t N = 0, max_producers = 0, flags = 0;
+  uint64_t** mirrors_dev = nullptr;          // [max_producers] pointers into producer mirrors
+  std::vector<void*> opened;                 // IPC mappings of mirrors to close
+  LaunchCtx* ctx = nullptr;
+  uint64_t items_base = 0;                   // copy-out launches only
+  uint32_t copy_ctas = 0, threads = 0, chunk_min = 0;
+  const uint32_t* crc = nullptr;
+  uint32_t sys = 1;
+};
+
+struct ring_peer_s {
+  int device = 0;
+  int ring_device = 0;
+  uint8_t* ring = nullptr;
+  bool ipc_opened = false;
+  DestState* st = nullptr;
+  DestDesc* desc_dev = nullptr;
+  DestDesc desc{};
+  LaunchCtx* ctx = nullptr;
+  uint64_t base = 0;
+  uint32_t copy_ctas = 0, threads = 0, chunk_min = 0, copy_mode = 0;
+  const uint32_t* crc = nullptr;
+};
+
+struct router_s {
+  int device = 0;
+  uint32_t max_routes = 0;
+  Route* routes_dev = nullptr;
+  std::vector<Route> routes;                 // host shadow (rr excluded)
+  DestDesc* dests_dev = nullptr;             // [kMaxRouterDests]
+  std::vector<ring_peer_t> dests;
+  LaunchCtx* ctx = nullptr;
+  uint64_t base = 0;
+  uint32_t copy_ctas = 0, threads = 0, chunk_min = 0;
+  const uint32_t* crc = nullptr;
+};
+
+extern "C" {
+
+const char* ring_strerror(ring_status_t s) {
+  switch (s) {
+    case RING_OK: return "ok";
+    case RING_EINVAL: return "invalid argument";
+    case RING_ENOMEM: return "out of device memory";
+    case RING_EMSGSIZE: return "message larger than the ring (or the copy-out buffer)";
+    case RING_FULL: return "ring full (try mode)";
+    case RING_EMPTY: return "ring empty (try mode)";
+    case RING_ETIMEDOUT: return "device spin timed out";
+    case RING_ECORRUPT: return "entry header checksum mismatch";
+    case RING_ECUDA: return "CUDA error";
+    case RING_EPEER: return "no peer access / IPC failure";
+    case RING_EPENDING: return "pending";
+  }
+  return "unknown";
+}
+const char* ring_last_cuda_error(void) { return g_cuda_err; }
+ring_status_t ring_set_timeout_ns(uint64_t ns) {
+  if (ns == 0) return RING_EINVAL;
+  g_timeout_ns = ns;
+  return RING_OK;
+}
+uint64_t ring_launch_count(void) { return g_launches.load(); }
+uint64_t ring_footprint(uint64_t len) { return footprint(len); }
+
+// ---- lifetime ------------------------------------------------------------------
+ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uint32_t max_producers,
+                          uint32_t flags, ring_t* out) {
+  if (!out || data_bytes == 0 || data_bytes % kAlign || data_bytes >= (1ull << 39) || n_slots == 0 ||
+      (n_slots & (n_slots - 1)) || n_slots > RING_MAX_SLOTS || max_producers == 0 ||
+      max_producers > RING_MAX_PRODUCERS)
+    return RING_EINVAL;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return RING_EINVAL;
+  DevGuard g(device);
+  ring_s* r = new ring_s;
+  r->device = device;
+  r->R = data_bytes;
+  r->N = n_slots;
+  r->max_producers = max_producers;
+  r->flags = flags;
+  r->sys = (flags & RING_CREATE_LOCAL) ? 0u : 1u;
+  r->data_off = data_offset(n_slots);
+  r->alloc = r->data_off + data_bytes;
+  cudaError_t e = cudaMalloc(&r->base, r->alloc);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete r;
+    return RING_ENOMEM;
+  }
+  // Only the control words and the size region need zeroing: entries are
+  // always written before they are published.
+  CUDA_TRY(cudaMemset(r->base, 0, r->data_off));
+  CUDA_TRY(cudaMalloc(&r->mirrors_dev, sizeof(uint64_t*) * max_producers));
+  CUDA_TRY(cudaMemset(r->mirrors_dev, 0, sizeof(uint64_t*) * max_producers));
+  CUDA_TRY(cudaMalloc(&r->ctx, sizeof(LaunchCtx)));
+  CUDA_TRY(cudaMemset(r->ctx, 0, sizeof(LaunchCtx)));
+  CUDA_TRY(cudaDeviceSynchronize());
+  ring_status_t s = crc_table_dev(device, &r->crc);
+  if (s != RING_OK) return s;
+  *out = r;
+  return RING_OK;
+}
+
+ring_status_t ring_destroy(ring_t r) {
+  if (!r) return RING_EINVAL;
+  DevGuard g(r->device);
+  cudaDeviceSynchronize();
+  for (void* p : r->opened) cudaIpcCloseMemHandle(p);
+  cudaFree(r->ctx);
+  cudaFree(r->mirrors_dev);
+  cudaFree(r->base);
+  delete r;
+  return RING_OK;
+}
+
+ring_status_t ring_get_info(ring_t r, ring_info_t* out) {
+  if (!r || !out) return RING_EINVAL;
+  out->device = r->device;
+  out->n_slots = r->N;
+  out->max_producers = r->max_producers;
+  out->data_bytes = r->R;
+  out->base = reinterpret_cast<uint64_t>(r->base);
+  out->data = reinterpret_cast<uint64_t>(r->base + r->data_off);
+  out->data_offset = r->data_off;
+  out->alloc_bytes = r->alloc;
+  return RING_OK;
+}
+
+ring_status_t ring_export(ring_t r, ring_handle_t* out) {
+  if (!r || !out) return RING_EINVAL;
+  HandleBlob b{};
+  b.magic = kMagicRing;
+  b.device = r->device;
+  b.pid = (int32_t)getpid();
+  b.token = g_token;
+  b.ptr = reinterpret_cast<uint64_t>(r->base);
+  b.R = r->R;
+  b.N = r->N;
+  b.max_producers = r->max_producers;
+  b.flags = r->flags;
+  DevGuard g(r->device);
+  CUDA_TRY(cudaIpcGetMemHandle(&b.ipc, r->base));
+  memset(out, 0, sizeof *out);
+  memcpy(out->bytes, &b, sizeof b);
+  return RING_OK;
+}
+
+ring_status_t ring_attach_peer(const ring_handle_t* h, int producer_device, uint32_t producer_id, ring_peer_t* out,
+                               ring_handle_t* mirror_out) {
+  if (!h || !out) return RING_EINVAL;
+  HandleBlob b;
+  memcpy(&b, h->bytes, sizeof b);
+  if (b.magic != kMagicRing || producer_id >= b.max_producers) return RING_EINVAL;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (producer_device < 0 || producer_device >= ndev) return RING_EINVAL;
+  const bool same_process = b.pid == (int32_t)getpid() && b.token == g_token;
+  if ((b.flags & RING_CREATE_LOCAL) && producer_device != b.device) return RING_EINVAL;
+  ring_peer_s* p = new ring_peer_s;
+  p->device = producer_device;
+  p->ring_device = b.device;
+  if (same_process) {
+    ring_status_t s = enable_peer(producer_device, b.device);
+    if (s != RING_OK) { delete p; return s; }
+    p->ring = reinterpret_cast<uint8_t*>(b.ptr);
+  } else {
+    DevGuard g(producer_device);
+    void* m = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&m, b.ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      snprintf(g_cuda_err, sizeof g_cuda_err, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+      cudaGetLastError();
+      delete p;
+      return RING_EPEER;
+    }
+    p->ring = static_cast<uint8_t*>(m);
+    p->ipc_opened = true;
+  }
+  DevGuard g(producer_device);
+  CUDA_TRY(cudaMalloc(&p->st, sizeof(DestState)));
+  CUDA_TRY(cudaMemset(p->st, 0, sizeof(DestState)));
+  // The channel starts where the ring is now (a ring may outlive producers).
+  uint64_t tail = 0;
+  CUDA_TRY(cudaMemcpy(&tail, p->ring + kTailOff, 8, cudaMemcpyDefault));
+  CUDA_TRY(cudaMemcpy(&p->st->tail_cache, &tail, 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMalloc(&p->ctx, sizeof(LaunchCtx)));
+  CUDA_TRY(cudaMemset(p->ctx, 0, sizeof(LaunchCtx)));
+  p->desc.ring = p->ring;
+  p->desc.data = p->ring + data_offset(b.N);
+  p->desc.st = p->st;
+  p->desc.R = b.R;
+  p->desc.N = b.N;
+  p->desc.mpsc = b.max_producers > 1 ? 1u : 0u;
+  p->desc.producer_id = producer_id;
+  p->desc.has_mirror = 0;
+  p->desc.sys = (same_process && producer_device == b.device) ? 0u : 1u;
+  CUDA_TRY(cudaMalloc(&p->desc_dev, sizeof(DestDesc)));
+  CUDA_TRY(cudaMemcpy(p->desc_dev, &p->desc, sizeof(DestDesc), cudaMemcpyHostToDevice));
+  ring_status_t s = crc_table_dev(producer_device, &p->crc);
+  if (s != RING_OK) return s;
+  if (mirror_out) {
+    HandleBlob mb{};
+    mb.magic = kMagicMirror;
+    mb.device = producer_device;
+    mb.pid = (int32_t)getpid();
+    mb.token = g_token;
+    mb.ptr = reinterpret_cast<uint64_t>(p->st);
+    mb.producer_id = producer_id;
+    CUDA_TRY(cudaIpcGetMemHandle(&mb.ipc, p->st));
+    memset(mirror_out, 0, sizeof *mirror_out);
+    memcpy(mirror_out->bytes, &mb, sizeof mb);
+  }
+  *out = p;
+  return RING_OK;
+}
+
+ring_status_t ring_bind_mirror(ring_t r, uint32_t producer_id, const ring_handle_t* mh) {
+  if (!r || !mh || producer_id >= r->max_producers) return RING_EINVAL;
+  HandleBlob b;
+  memcpy(&b, mh->bytes, sizeof b);
+  if (b.magic != kMagicMirror || b.producer_id != producer_id) return RING_EINVAL;
+  const bool same_process = b.pid == (int32_t)getpid() && b.token == g_token;
+  uint64_t* mirror = nullptr;
+  if (same_process) {
+    ring_status_t s = enable_peer(r->device, b.device);
+    if (s != RING_OK) return s;
+    mirror = reinterpret_cast<uint64_t*>(b.ptr);   // DestState::mirror_head is at offset 0
+  } else {
+    DevGuard g(r->device);
+    void* m = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&m, b.ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      snprintf(g_cuda_err, sizeof g_cuda_err, "cudaIpcOpenMemHandle(mirror): %s", cudaGetErrorString(e));
+      cudaGetLastError();
+      return RING_EPEER;
+    }
+    r->opened.push_back(m);
+    mirror = static_cast<uint64_t*>(m);
+  }
+  DevGuard g(r->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  uint64_t head = 0;
+  CUDA_TRY(cudaMemcpy(&head, r->base + kHeadOff, 8, cudaMemcpyDeviceToHost));
+  head |= kMirrorValid;
+  CUDA_TRY(cudaMemcpy(mirror, &head, 8, cudaMemcpyDefault));
+  CUDA_TRY(cudaMemcpy(r->mirrors_dev + producer_id, &mirror, sizeof mirror, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return RING_OK;
+}
+
+ring_status_t ring_detach(ring_peer_t p) {
+  if (!p) return RING_EINVAL;
+  DevGuard g(p->device);
+  cudaDeviceSynchronize();
+  if (p->ipc_opened) cudaIpcCloseMemHandle(p->ring);
+  cudaFree(p->desc_dev);
+  cudaFree(p->ctx);
+  cudaFree(p->st);
+  delete p;
+  return RING_OK;
+}
+
+// ---- producer ----------------------------------------------------------------------
+ring_status_t ring_peer_config(ring_peer_t p, uint32_t copy_ctas, uint32_t threads, uint32_t copy_mode) {
+  if (!p || copy_ctas > 1023 || (threads && (threads % 32 || threads > 1024 || threads < 64)) || copy_mode > 1)
+    return RING_EINVAL;
+  p->copy_ctas = copy_ctas;
+  p->threads = threads;
+  p->copy_mode = copy_mode;
+  return RING_OK;
+}
+
+uint64_t ring_peer_submitted(ring_peer_t p) { return p ? p->base : 0; }
+
+static void default_put_config(int device, bool sys, uint32_t* ctas, uint32_t* threads, uint32_t* chunk) {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  // NVLink: ~32 SMs of 16-B stores saturate the peer link (tools/probe2 on
+  // B200: 678-695 GB/s from 32 CTAs up); HBM->HBM: every SM but the control one.
+  if (!*ctas) *ctas = sys ? 32u : (uint32_t)(nsm - 1);
+  if (!*threads) *threads = 512;
+  if (!*chunk) *chunk = 64u << 10;
+}
+
+static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const ring_msg_t* inline_msg, uint32_t n,
+                                uint32_t flags, uint32_t* d_status, void* stream) {
+  if (!p || !d_status || n == 0 || (!d_msgs && !inline_msg)) return RING_EINVAL;
+  PutArgs a{};
+  if (inline_msg) a.inline_msg = *inline_msg;
+  a.msgs = d_msgs;
+  a.status = d_status;
+  a.ctx = p->ctx;
+  a.dests = p->desc_dev;
+  a.n_dests = 1;
+  a.crc_table = p->crc;
+  a.base = p->base;
+  a.timeout_ns = g_timeout_ns;
+  a.n = n;
+  a.flags = flags;
+  uint32_t ctas = p->copy_ctas, thr = p->threads, chunk = p->chunk_min;
+  DevGuard g(p->device);
+  default_put_config(p->device, p->desc.sys, &ctas, &thr, &chunk);
+  a.copy_ctas = ctas;
+  a.chunk_min = chunk;
+  a.copy_mode = p->copy_mode;
+  CUDA_TRY(launch_put(a, thr, as_stream(stream)));
+  p->base += n;
+  g_launches++;
+  return RING_OK;
+}
+
+ring_status_t ring_put_batch(ring_peer_t p, const ring_msg_t* d_msgs, uint32_t n, uint32_t flags, uint32_t* d_status,
+                             void* stream) {
+  return put_common(p, d_msgs, nullptr, n, flags, d_status, stream);
+}
+
+ring_status_t ring_put(ring_peer_t p, const void* d_payload, uint64_t len, const ring_hdr_t* hdr, uint32_t flags,
+                       uint32_t* d_status, void* stream) {
+  if (!hdr || (!d_payload && len)) return RING_EINVAL;
+  ring_msg_t m{};
+  m.src = reinterpret_cast<uint64_t>(d_payload);
+  m.len = len;
+  m.hdr = *hdr;
+  return put_common(p, nullptr, &m, 1, flags, d_status, stream);
+}
+
+// ---- consumer ----------------------------------------------------------------------
+ring_status_t ring_config(ring_t r, uint32_t copy_ctas, uint32_t threads) {
+  if (!r || copy_ctas > 1023 || (threads && (threads % 32 || threads > 1024 || threads < 64))) return RING_EINVAL;
+  r->copy_ctas = copy_ctas;
+  r->threads = threads;
+  return RING_OK;
+}
+
+static ring_status_t get_common(ring_t r, uint32_t n, ring_view_t* d_views, void* d_dst, uint64_t dst_stride,
+                                uint32_t flags, uint32_t consume, void* stream) {
+  if (!r || !d_views || n == 0 || (d_dst && dst_stride == 0)) return RING_EINVAL;
+  GetArgs a{};
+  a.ring = r->base;
+  a.data = r->base + r->data_off;
+  a.views = d_views;
+  a.dst = static_cast<uint8_t*>(d_dst);
+  a.mirrors = r->mirrors_dev;
+  a.ctx = r->ctx;
+  a.crc_table = r->crc;
+  a.R = r->R;
+  a.dst_stride = dst_stride;
+  a.base = r->items_base;
+  a.timeout_ns = g_timeout_ns;
+  a.N = r->N;
+  a.n = n;
+  a.flags = flags;
+  a.consume = consume;
+  a.sys = r->sys;
+  a.n_mirrors = r->max_producers;
+  DevGuard g(r->device);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, r->device);
+  a.copy_ctas = r->copy_ctas ? r->copy_ctas : (uint32_t)(nsm - 1);
+  a.chunk_min = r->chunk_min ? r->chunk_min : (64u << 10);
+  CUDA_TRY(launch_get(a, r->threads ? r->threads : 512, as_stream(stream)));
+  if (d_dst) r->items_base += n;
+  g_launches++;
+  return RING_OK;
+}
+
+ring_status_t ring_get(ring_t r, uint32_t n, ring_view_t* d_views, void* d_dst, uint64_t dst_stride, uint32_t flags,
+                       void* stream) {
+  return get_common(r, n, d_views, d_dst, dst_stride, flags, 0, stream);
+}
+
+ring_status_t ring_consume(ring_t r, uint32_t n, ring_view_t* d_views, void* d_dst, uint64_t dst_stride,
+                           uint32_t flags, void* stream) {
+  return get_common(r, n, d_views, d_dst, dst_stride, flags, 1, stream);
+}
+
+ring_status_t ring_release(ring_t r, uint32_t count, void* stream) {
+  if (!r) return RING_EINVAL;
+  ReleaseArgs a{};
+  a.ring = r->base;
+  a.mirrors = r->mirrors_dev;
+  a.R = r->R;
+  a.N = r->N;
+  a.count = count;
+  a.sys = r->sys;
+  a.n_mirrors = r->max_producers;
+  DevGuard g(r->device);
+  CUDA_TRY(launch_release(a, as_stream(stream)));
+  g_launches++;
+  return RING_OK;
+}
+
+ring_status_t ring_read_image(ring_t r, uint64_t* lock, uint64_t* tail, uint64_t* head, uint64_t* cursor,
+                              uint64_t* slots) {
+  if (!r) return RING_EINVAL;
+  DevGuard g(r->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  uint64_t w[4];
+  CUDA_TRY(cudaMemcpy(&w[0], r->base + kLockOff, 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&w[1], r->base + kTailOff, 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&w[2], r->base + kHeadOff, 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&w[3], r->base + kCursorOff, 8, cudaMemcpyDeviceToHost));
+  if (lock) *lock = w[0];
+  if (tail) *tail = w[1];
+  if (head) *head = w[2];
+  if (cursor) *cursor = w[3];
+  if (slots) CUDA_TRY(cudaMemcpy(slots, r->base + kSlotsOff, 8ull * r->N, cudaMemcpyDeviceToHost));
+  return RING_OK;
+}
+
+ring_status_t ring_read_data(ring_t r, uint64_t offset, uint64_t len, void* host_dst) {
+  if (!r || (len && !host_dst) || offset > r->R || len > r->R - offset) return RING_EINVAL;
+  DevGuard g(r->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (len) CUDA_TRY(cudaMemcpy(host_dst, r->base + r->data_off + offset, len, cudaMemcpyDeviceToHost));
+  return RING_OK;
+}
+
+ring_status_t ring_write_data(ring_t r, uint64_t offset, uint64_t len, const void* host_src) {
+  if (!r || (len && !host_src) || offset > r->R || len > r->R - offset) return RING_EINVAL;
+  DevGuard g(r->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (len) CUDA_TRY(cudaMemcpy(r->base + r->data_off + offset, host_src, len, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return RING_OK;
+}
+
+// ---- router ------------------------------------------------------------------------
+ring_status_t router_create(int device, uint32_t max_routes, router_t* out) {
+  if (!out || max_routes == 0 || max_routes > 4096) return RING_EINVAL;
+  DevGuard g(device);
+  router_s* r = new router_s;
+  r->device = device;
+  r->max_routes = max_routes;
+  r->routes.resize(max_routes);
+  memset(r->routes.data(), 0, sizeof(Route) * max_routes);
+  CUDA_TRY(cudaMalloc(&r->routes_dev, sizeof(Route) * max_routes));
+  CUDA_TRY(cudaMemset(r->routes_dev, 0, sizeof(Route) * max_routes));
+  CUDA_TRY(cudaMalloc(&r->dests_dev, sizeof(DestDesc) * kMaxRouterDests));
+  CUDA_TRY(cudaMemset(r->dests_dev, 0, sizeof(DestDesc) * kMaxRouterDests));
+  CUDA_TRY(cudaMalloc(&r->ctx, sizeof(LaunchCtx)));
+  CUDA_TRY(cudaMemset(r->ctx, 0, sizeof(LaunchCtx)));
+  ring_status_t s = crc_table_dev(device, &r->crc);
+  if (s != RING_OK) return s;
+  *out = r;
+  return RING_OK;
+}
+
+ring_status_t router_destroy(router_t r) {
+  if (!r) return RING_EINVAL;
+  DevGuard g(r->device);
+  cudaDeviceSynchronize();
+  cudaFree(r->ctx);
+  cudaFree(r->dests_dev);
+  cudaFree(r->routes_dev);
+  delete r;
+  return RING_OK;
+}
+
+ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, const ring_peer_t* dests, uint32_t n,
+                               void* stream) {
+  if (!r || n > kMaxDests || (n && !dests)) return RING_EINVAL;
+  DevGuard g(r->device);
+  Route nr{};
+  nr.app_id = app_id;
+  nr.stage = stage;
+  nr.n = (uint16_t)n;
+  for (uint32_t i = 0; i < n; ++i) {
+    ring_peer_t p = dests[i];
+    if (!p || p->device != r->device) return RING_EINVAL;
+    uint32_t idx = 0;
+    while (idx < r->dests.size() && r->dests[idx] != p) ++idx;
+    if (idx == r->dests.size()) {
+      if (idx >= (uint32_t)kMaxRouterDests) return RING_EINVAL;
+      r->dests.push_back(p);
+      CUDA_TRY(cudaMemcpyAsync(r->dests_dev + idx, &p->desc, sizeof(DestDesc), cudaMemcpyHostToDevice, as_stream(stream)));
+      CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+    }
+    nr.dests[i] = idx;
+  }
+  uint32_t slot = r->max_routes;
+  for (uint32_t i = 0; i < r->max_routes; ++i)
+    if (r->routes[i].n && r->routes[i].app_id == app_id && r->routes[i].stage == stage) { slot = i; break; }
+  if (slot == r->max_routes)
+    for (uint32_t i = 0; i < r->max_routes; ++i)
+      if (!r->routes[i].n) { slot = i; break; }
+  if (slot == r->max_routes) return RING_EINVAL;
+  nr.epoch = r->routes[slot].epoch + 1;     // epoch flip (NodeManager reassignment)
+  r->routes[slot] = nr;
+  // Write everything but the device-owned rr counter, in stream order with the
+  // caller's puts: launched puts finish to the old destination.
+  static thread_local Route staged;
+  staged = nr;
+  Route* d = r->routes_dev + slot;
+  CUDA_TRY(cudaMemcpyAsync(d, &staged, offsetof(Route, rr), cudaMemcpyHostToDevice, as_stream(stream)));
+  CUDA_TRY(cudaMemcpyAsync(&d->dests, &staged.dests, sizeof(staged.dests), cudaMemcpyHostToDevice, as_stream(stream)));
+  CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+  return RING_OK;
+}
+
+ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, uint32_t flags, uint32_t* d_status,
+                              uint32_t* d_dest, void* stream) {
+  if (!r || !d_msgs || !d_status || n == 0) return RING_EINVAL;
+  if (r->dests.empty()) return RING_EINVAL;
+  PutArgs a{};
+  a.msgs = d_msgs;
+  a.status = d_status;
+  a.dest_out = d_dest;
+  a.ctx = r->ctx;
+  a.dests = r->dests_dev;
+  a.n_dests = (uint32_t)r->dests.size();
+  a.routes = r->routes_dev;
+  a.n_routes = r->max_routes;
+  a.crc_table = r->crc;
+  a.base = r->base;
+  a.timeout_ns = g_timeout_ns;
+  a.n = n;
+  a.flags = flags;
+  bool sys = false;
+  for (auto* p : r->dests) sys = sys || p->desc.sys;
+  uint32_t ctas = r->copy_ctas, thr = r->threads, chunk = r->chunk_min;
+  DevGuard g(r->device);
+  default_put_config(r->device, sys, &ctas, &thr, &chunk);
+  a.copy_ctas = ctas;
+  a.chunk_min = chunk;
+  CUDA_TRY(launch_put(a, thr, as_stream(stream)));
+  r->base += n;
+  g_launches++;
+  return RING_OK;
+}
+
+}  // extern "C"

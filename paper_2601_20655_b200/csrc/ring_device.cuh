@@ -1,0 +1,151 @@
+// ring_device.cuh — device-side layout, word packing and memory-ordering
+// primitives of the B200 double ring (sm_100a).
+//
+// Layout ("lock region, fixed-length header
+// with head and tail, buffer region, size region"):
+//   [0,128)   lock  u64   0 = free, producer_id+1 = held          (R14)
+//   [128,256) tail  u64   (P_b << 24) | P_seq                      (R8, R5)
+//   [256,384) head  u64   (H_b << 24) | H_seq
+//   [384,512) read cursor G u64 (consumer private)
+//   [512, 512+8N) size slots u64: busy<<63 | pad<<62 | footprint   (R9, R3)
+//   [D, D+R)  buffer region, D = align_up(512 + 8N, 4096)
+#pragma once
+#include <cstdint>
+
+namespace b200ring {
+
+constexpr uint64_t kLockOff = 0;
+constexpr uint64_t kTailOff = 128;
+constexpr uint64_t kHeadOff = 256;
+constexpr uint64_t kCursorOff = 384;
+constexpr uint64_t kSlotsOff = 512;
+constexpr uint64_t kAlign = 128;     // entry alignment (R11)
+constexpr uint64_t kHdr = 64;        // entry header bytes (R11)
+constexpr uint64_t kBusy = 1ull << 63;
+constexpr uint64_t kPad = 1ull << 62;
+constexpr uint64_t kFMask = (1ull << 62) - 1;
+constexpr uint32_t kSeqMask = (1u << 24) - 1;
+constexpr int kPlanRing = 64;        // in-flight messages per launch context
+constexpr int kMaxDests = 8;          // destinations per route
+constexpr int kMaxRouterDests = 32;   // destinations per launch (bit mask)
+
+__host__ __device__ inline uint64_t data_offset(uint32_t n_slots) {
+  return (kSlotsOff + 8ull * n_slots + 4095ull) & ~4095ull;
+}
+// f = align_up(64 + len, 128)  (R9)
+__host__ __device__ inline uint64_t footprint(uint64_t len) { return (kHdr + len + kAlign - 1) & ~(kAlign - 1); }
+// P_b update, PAPER.md:731-739 (strict '<': exact fit wraps to 0)
+__host__ __device__ inline uint64_t advance(uint64_t p_b, uint64_t f, uint64_t R) { return p_b + f < R ? p_b + f : 0; }
+__host__ __device__ inline uint32_t seq_inc(uint32_t q) { return (q + 1) & kSeqMask; }  // PAPER.md:741-745 (R5)
+__host__ __device__ inline uint64_t pack_ptr(uint64_t b, uint32_t q) { return (b << 24) | (q & kSeqMask); }
+__host__ __device__ inline uint64_t ptr_off(uint64_t w) { return w >> 24; }
+__host__ __device__ inline uint32_t ptr_seq(uint64_t w) { return (uint32_t)(w & kSeqMask); }
+__host__ __device__ inline uint32_t seq_dist(uint32_t p, uint32_t h) { return (p - h) & kSeqMask; }
+
+// Space rule (R4): can [p_b, p_b+f) (p_b+f <= R) be written without touching
+// the live range [h_b, p_b) of unreleased entries?
+__host__ __device__ inline bool span_free(uint64_t p_b, uint32_t p_q, uint64_t h_b, uint32_t h_q, uint64_t f) {
+  if (p_q == h_q) return true;          // empty
+  if (p_b > h_b) return true;           // live range does not wrap
+  if (p_b < h_b) return p_b + f <= h_b; // live range wraps: free gap is [p_b, h_b)
+  return false;                         // same offset, non-empty: full
+}
+
+// ---------------------------------------------------------------------------
+// Memory-ordering primitives.  Scope is a template parameter: rings whose
+// producer and consumer sit on one GPU use .gpu (MEMBAR.GPU, ~0.4 us); rings
+// crossing NVLink use .sys (MEMBAR.SYS, ~1.7 us measured on B200).
+// ---------------------------------------------------------------------------
+template <bool SYS>
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  if (SYS) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+template <bool SYS>
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  if (SYS) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+template <bool SYS>
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  if (SYS) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  if (SYS) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ void fence_acq_rel() {
+  if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+template <bool SYS>
+__device__ __forceinline__ uint64_t cas_acquire(uint64_t* p, uint64_t cmp, uint64_t val) {
+  uint64_t old;
+  if (SYS) asm volatile("atom.acquire.sys.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(val) : "memory");
+  else asm volatile("atom.acquire.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(val) : "memory");
+  return old;
+}
+// Launch-local coordination (all on the producer's own GPU): gpu scope.
+__device__ __forceinline__ uint64_t ld_acquire_gpu64(const uint64_t* p) { return ld_acquire<false>(p); }
+__device__ __forceinline__ uint32_t ld_acquire_gpu32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu64(uint64_t* p, uint64_t v) { st_release<false>(p, v); }
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// Streaming 16-byte copies through integer registers only (R17: bit-exact,
+// NaN payloads preserved).  Loads bypass L1 (read once).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int4 ld_stream16(const void* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st16(void* p, int4 v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Warp-parallel CRC-32/IEEE of the 52 header bytes [4,56) (R10).
+// CRC is affine over GF(2): crc(m) = crc(0^52) ^ XOR_{set bits (p,b)} T[p][b],
+// with T[p][b] the CRC register contribution of bit b of byte p.  The table
+// (416 words, layout [bit 0..31][word 0..12], then C0 = crc(0^52)) is built on
+// the host by host.cpp from its own bitwise CRC and passed to the kernels.
+// `w` = lane l's header word l+1 (bytes 4(l+1)..4(l+1)+3) for l < 13.
+// ---------------------------------------------------------------------------
+constexpr int kCrcWords = 13;
+constexpr int kCrcTableWords = 32 * kCrcWords + 1;
+__device__ __forceinline__ uint32_t warp_crc52(uint32_t w, int lane, const uint32_t* __restrict__ table) {
+  uint32_t acc = 0;
+  if (lane < kCrcWords) {
+#pragma unroll 8
+    for (int b = 0; b < 32; ++b) {
+      uint32_t t = __ldg(table + b * kCrcWords + lane);
+      acc ^= t & (0u - ((w >> b) & 1u));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc ^ __ldg(table + 32 * kCrcWords);
+}
+
+}  // namespace b200ring

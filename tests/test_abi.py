@@ -1,0 +1,83 @@
+"""CPU-only checks of the C-ABI boundary: the in-tree library builds, loads and
+exports every entry point include/b200ring.h declares; host-side validation
+and pure helpers answer without a GPU (no compute calls)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "b200ring.h")
+
+
+def declared_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*([a-z_0-9]+)\s*\(", txt, flags=re.M)
+    return sorted(set(n for n in names if n.startswith(("ring_", "router_"))))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2601_20655_b200 import build
+    build.build()
+    from paper_2601_20655_b200 import ring
+    return ring
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ["ring_create", "ring_attach_peer", "ring_put", "ring_get", "ring_release", "ring_destroy",
+              "ring_export", "ring_bind_mirror", "ring_put_batch", "ring_consume", "router_set_route",
+              "ring_put_routed"]:
+        assert n in names
+    assert len(names) >= 25
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (\w+)$", out, flags=re.M))
+    missing = [n for n in declared_functions() if n not in exported]
+    assert not missing, missing
+    so = ctypes.CDLL(lib.LIB_PATH)
+    for n in declared_functions():
+        getattr(so, n)
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_pure_helpers_without_gpu(lib):
+    assert lib.ring_footprint(0) == 128
+    assert lib.ring_footprint(4096) == 4224
+    assert lib.ring_footprint(1048512) == 1 << 20
+    assert lib.ring_strerror(lib.RING_ECORRUPT).startswith("entry header checksum")
+
+
+def test_host_validation_rejects_bad_geometry(lib):
+    for args in [(0, 0, 8), (0, 1000, 8), (0, 1 << 20, 6), (0, 1 << 20, 0), (0, 1 << 20, 1 << 24)]:
+        with pytest.raises(lib.RingError) as e:
+            lib.ring_create(*args)
+        assert e.value.status == lib.RING_EINVAL
+    with pytest.raises(lib.RingError) as e:
+        lib.ring_create(0, 1 << 20, 8, 0)
+    assert e.value.status == lib.RING_EINVAL
+
+
+def test_binding_has_no_fallback(lib):
+    """The product package never imports the oracle, and the binding loads only
+    the in-tree CUDA library."""
+    pkg = os.path.join(ROOT, "paper_2601_20655_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, flags=re.M), f
+                assert not re.search(r"#\s*include\s*[<\"].*oracle", src), f
+                assert "import synth" not in src and "from synth" not in src, f
+    assert lib.LIB_PATH.startswith(pkg)
