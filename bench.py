@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Benchmark of the double-ring tensor transport (BASELINE.json metric:
-"ring transfer GB/s per GPU vs 900 GB/s NVLink; p50/p99 msg latency").
+"ring transfer GB/s per GPU vs 900 GB/s NVLink; p50/p99 msg latency at 1/2/4/8 GPU").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
@@ -10,11 +10,13 @@ N = 1 -> BASELINE.json configs[1] (C2): a same-GPU ring of 64 slots x 1 MiB
 pass of the whole hot path over one batch: ring_put_batch of 64 messages
 (claim, header + CRC, copy, publish) then ring_consume of the 64 entries (poll,
 slot + header read, CRC verify, release + credit), in stream order on one GPU
-(two kernels spinning on each other must never share a GPU; R20).
+(two kernels spinning on each other must never share a GPU).
 N >= 2 -> C3-shaped messages (umT5 embeddings 4,194,304 B / 480p latents
 4,193,280 B, alternating) over NVLink: rank r puts into the ring on rank
 (r+1) % N while consuming its own ring (fed by rank r-1), both streaming
 concurrently with credit flowing back; weak scaling (fixed work per GPU).
+Handles are exchanged over a gloo group of torch.distributed (plumbing only:
+no collective and no NCCL on the data path).
 
 Prints ONE JSON line on rank 0.  `value` = payload bytes delivered by all
 ranks / max-over-ranks device time of the K timed steps.
@@ -39,6 +41,11 @@ METRIC = "ring transfer GB/s per GPU vs 900 GB/s NVLink; p50/p99 msg latency at 
 UNIT = "GB/s"
 NVLINK_PEAK_MEASURED = 770.0   # B200_PROFILING.md: measured peer copy, per direction per GPU
 NVLINK_NOMINAL = 900.0
+C3_LENS = (4194304, 4193280)   # umT5 embeddings 512x4096 bf16 / 480p latents 16x21x60x104 bf16
+
+
+def log(*a):
+    print(f"[bench r{os.environ.get('RANK', '0')} {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
 
 
 def load_peaks():
@@ -47,6 +54,10 @@ def load_peaks():
             return json.load(f), "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def pct(x, q):
+    return round(float(np.percentile(np.asarray(x, dtype=np.float64), q)), 2) if len(x) else None
 
 
 # ---------------------------------------------------------------------------------------
@@ -100,26 +111,34 @@ class Clocks:
 # ---------------------------------------------------------------------------------------
 # CPU baseline: the oracle as it stands on the host cores (bounded sample)
 # ---------------------------------------------------------------------------------------
-def oracle_throughput(payload_lens, R_bytes, N_slots, budget_s: float = 12.0, seed: int = 0):
-    """Run the CPU oracle (oracle/ring.py, one producer, draining consumer) over
-    repeated batches of the workload's messages for about `budget_s` seconds.
-    Returns (GB/s of payload, messages, seconds)."""
+def oracle_inputs(payload_lens, seed: int = 0):
     import synth
-    from oracle.ring import Layout, Sim, Msg, run
-    L = Layout(R_bytes, N_slots)
-    payloads = [synth.payload_bytes(synth.SEED_BASE + seed, 0, q, n).tobytes() for q, n in enumerate(payload_lens)]
-    msgs = [Msg(n, p, bytes(16), 0, 7, 1) for n, p in zip(payload_lens, payloads)]
+    from oracle.ring import Msg
+    return [Msg(n, synth.payload_bytes(synth.SEED_BASE + seed, 0, q, n).tobytes(), bytes(16), 0, 7, 1)
+            for q, n in enumerate(payload_lens)]
+
+
+def oracle_pass(msgs, R_bytes, N_slots):
+    """One pass of the CPU oracle (oracle/ring.py: one producer, draining consumer)."""
+    from oracle.ring import Layout, Sim, run
+    sim = Sim(Layout(R_bytes, N_slots), {0: msgs}, mpsc=False, block=True, depth=1, check=False)
+    run(sim, policy="drain")
+    return sim
+
+
+def cpu_baseline(payload_lens, R_bytes, N_slots, budget_s: float):
+    msgs = oracle_inputs(payload_lens)
     t0 = time.perf_counter()
-    done_msgs = done_bytes = 0
+    n = 0
     while True:
-        sim = Sim(L, {0: msgs}, mpsc=False, block=True, depth=1, check=False)
-        run(sim, policy="drain")
-        done_msgs += len(msgs)
-        done_bytes += sum(payload_lens)
+        oracle_pass(msgs, R_bytes, N_slots)
+        n += 1
         dt = time.perf_counter() - t0
         if dt >= budget_s:
             break
-    return done_bytes / dt / 1e9, done_msgs, dt
+    return {"value": round(sum(payload_lens) * n / dt / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} x {len(payload_lens)} messages of {payload_lens[0]:,} B through oracle/ring.py "
+                      f"(R={R_bytes >> 20} MiB, N={N_slots}), single thread, {dt:.1f} s"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -138,14 +157,12 @@ def bench_c2(args):
     ring = R.ring_create(dev, Rb, N, 1, R.RING_CREATE_LOCAL)
     peer, mh = R.ring_attach_peer(R.ring_export(ring), dev, 0)
     R.ring_bind_mirror(ring, 0, mh)
-    if args.copy_ctas or args.threads:
-        R.ring_peer_config(peer, args.copy_ctas, args.threads, 0)
+    if args.ctas or args.threads:
+        R.ring_peer_config(peer, args.ctas, args.threads, 0)
     stride = (plen + 255) // 256 * 256
     src = torch.empty(sets * m * stride, dtype=torch.uint8, device="cuda")
-    for s in range(sets):
-        for q in range(m):
-            k = s * m + q
-            src[k * stride: k * stride + plen] = torch.from_numpy(synth.payload_bytes(synth.SEED_BASE + 2, 0, k, plen))
+    for k in range(sets * m):
+        src[k * stride: k * stride + plen] = torch.from_numpy(synth.payload_bytes(synth.SEED_BASE + 2, 0, k, plen))
     d_msgs = []
     for s in range(sets):
         srcs = [src.data_ptr() + (s * m + q) * stride for q in range(m)]
@@ -172,10 +189,9 @@ def bench_c2(args):
         step(i)
     torch.cuda.synchronize()
     assert (status == 0).all().item(), "put failed in warm-up"
-    v = R.parse_views(views.cpu().numpy())
-    assert (v["status"] == 0).all(), "consume failed in warm-up"
+    assert (R.parse_views(views.cpu().numpy())["status"] == 0).all(), "consume failed in warm-up"
 
-    clk = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0]) if False else dev)
+    clk = Clocks(dev)
     clk.start()
     l0 = R.ring_launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -193,7 +209,6 @@ def bench_c2(args):
     assert (status == 0).all().item()
     v = R.parse_views(views.cpu().numpy())
     assert (v["status"] == 0).all()
-    # latency of the last step's messages: t_visible - t_put (same GPU clock)
     t_put = np.frombuffer(v["header"][:, 56:64].tobytes(), dtype="<u8")
     lat_us = (v["t_visible"].astype(np.int64) - t_put.astype(np.int64)) / 1e3
 
@@ -210,24 +225,24 @@ def bench_c2(args):
     host_src.copy_(src[: m * stride].cpu())
     host_views = torch.empty(m * 128, dtype=torch.uint8).pin_memory()
     e_steps = max(3, min(args.steps, 50))
-    for i in range(2):
+
+    def e2e_step():
         src[: m * stride].copy_(host_src, non_blocking=True)
         step(0)
         host_views.copy_(views, non_blocking=True)
+
+    for i in range(2):
+        e2e_step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(e_steps):
-        src[: m * stride].copy_(host_src, non_blocking=True)
-        step(0)
-        host_views.copy_(views, non_blocking=True)
+        e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    e2e = m * plen * e_steps / (e2e_ms / 1e3) / 1e9
+    e2e = m * plen * e_steps / (e0.elapsed_time(e1) / 1e3) / 1e9
 
-    cpu_gbs, cpu_msgs, cpu_s = oracle_throughput([plen] * m, Rb, N, budget_s=args.cpu_budget)
-
+    cpu = cpu_baseline([plen] * 16, Rb, N, args.cpu_budget)
     R.ring_detach(peer)
     R.ring_destroy(ring)
     return {
@@ -240,9 +255,9 @@ def bench_c2(args):
                    "l2": "inputs larger than L2 (4 x 64 MiB rotating source sets + 64 MiB ring)",
                    "consume_mode": "view (zero copy)", "parallelism": "replicas only (1 ring)"},
         "msgs_per_s": round(m * args.steps / (ms / 1e3), 1),
-        "latency_us": {"p50": round(float(np.percentile(lat_us, 50)), 2),
-                       "p99": round(float(np.percentile(lat_us, 99)), 2),
-                       "what": "t_visible - t_put of the last step's 64 messages (batched put: includes queueing)"},
+        "latency_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99),
+                       "what": "t_visible - t_put of the last step's 64 messages (same GPU clock; batched put, "
+                               "so it includes the wait behind earlier messages of the batch)"},
         "kernels_ms": {"put_avg": round(put_avg_ms, 5), "consume_avg": round(statistics.mean(get_ms), 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
@@ -252,16 +267,14 @@ def bench_c2(args):
                 "d2h_bytes_per_step": m * 128},
         "gpu_launches": int(launches),
         "clocks": clocks,
-        "cpu_baseline": {"value": round(cpu_gbs, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{cpu_msgs} x 1,048,512-B messages through the Python oracle ring "
-                                   f"(R=64 MiB, N=64) in {cpu_s:.1f} s"},
+        "cpu_baseline": cpu,
     }
 
 
 # ---------------------------------------------------------------------------------------
 # N >= 2: ring of pairs over NVLink (C3-shaped messages)
 # ---------------------------------------------------------------------------------------
-def bench_pairs(args, rank, world):
+def bench_pairs(args, rank, world, grp):
     import torch
     import torch.distributed as dist
     import synth
@@ -271,20 +284,19 @@ def bench_pairs(args, rank, world):
     torch.cuda.set_device(dev)
     Rb, N = 64 << 20, 64
     m = args.msgs_per_step or 32
-    lens = [synth.wan_bytes("umt5_emb"), synth.wan_bytes("latent_480p")]
     ring = R.ring_create(dev, Rb, N, 1, 0)
     handles = [None] * world
-    dist.all_gather_object(handles, R.ring_export(ring))
-    nxt = (rank + 1) % world
-    peer, mh = R.ring_attach_peer(handles[nxt], dev, 0)
-    if args.copy_ctas or args.threads:
-        R.ring_peer_config(peer, args.copy_ctas, args.threads, 0)
+    dist.all_gather_object(handles, R.ring_export(ring), group=grp)
+    peer, mh = R.ring_attach_peer(handles[(rank + 1) % world], dev, 0)
+    if args.ctas or args.threads:
+        R.ring_peer_config(peer, args.ctas, args.threads, 0)
     mirrors = [None] * world
-    dist.all_gather_object(mirrors, mh)
+    dist.all_gather_object(mirrors, mh, group=grp)
     R.ring_bind_mirror(ring, 0, mirrors[(rank - 1) % world])
-    dist.barrier()
-    sets = 2
-    stride = 4194304
+    offsets = [None] * world
+    dist.all_gather_object(offsets, R.ring_clock_offset_ns(dev), group=grp)
+    log("rings attached; clock offsets (gpu - host, ns):", offsets)
+    sets, stride = 2, 4194304
     src = torch.empty(sets * m * stride, dtype=torch.uint8, device="cuda")
     d_msgs = []
     for s in range(sets):
@@ -300,24 +312,32 @@ def bench_pairs(args, rank, world):
         hdr = [synth.header_fields(synth.SEED_BASE + 3, rank, s * m + q) for q in range(m)]
         a = R.make_msgs(srcs, ln, [h[0] for h in hdr], [h[1] for h in hdr], [7] * m, [2] * m)
         d_msgs.append(torch.from_numpy(a.view(np.uint8).copy()).cuda())
-    payload_step = sum(lens[q % 2] for q in range(m))
+    payload_step = sum(C3_LENS[q % 2] for q in range(m))
     status = torch.zeros(m, dtype=torch.int32, device="cuda")
     views = torch.zeros(m * 128, dtype=torch.uint8, device="cuda")
-    sp = torch.cuda.Stream()
-    sc = torch.cuda.Stream()
+    sp, sc = torch.cuda.Stream(), torch.cuda.Stream()
 
     def step(i):
-        R.ring_consume(ring, m, views, None, 0, 0, sc)
+        R.ring_consume(ring, m, views, None, 0, 0, sc)     # consumer first: it waits for data
         R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
+
+    def latencies():
+        v = R.parse_views(views.cpu().numpy())
+        t_put = np.frombuffer(v["header"][:, 56:64].tobytes(), dtype="<u8").astype(np.int64)
+        prev = (rank - 1) % world
+        # both stamps on the host clock: t - offset(gpu)
+        return (((v["t_visible"].astype(np.int64) - offsets[rank]) - (t_put - offsets[prev])) / 1e3).tolist(), v
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    dist.barrier()
+    ok_w = bool((status == 0).all().item()) and bool((latencies()[1]["status"] == 0).all())
+    log("warm-up done, ok =", ok_w)
+    dist.barrier(group=grp)
     clk = Clocks(dev) if rank == 0 else None
     if clk:
         clk.start()
-    dist.barrier()
+    dist.barrier(group=grp)
     torch.cuda.synchronize()
     l0 = R.ring_launch_count()
     t0c, t0p = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -331,26 +351,69 @@ def bench_pairs(args, rank, world):
     torch.cuda.synchronize()
     launches = R.ring_launch_count() - l0
     ms = max(t0c.elapsed_time(t1c), t0p.elapsed_time(t1p), t0c.elapsed_time(t1p), t0p.elapsed_time(t1c))
-    dist.barrier()
+    dist.barrier(group=grp)
     clocks = clk.stop() if clk else None
-    ok = bool((status == 0).all().item()) and bool((R.parse_views(views.cpu().numpy())["status"] == 0).all())
-    v = R.parse_views(views.cpu().numpy())
-    t_put = np.frombuffer(v["header"][:, 56:64].tobytes(), dtype="<u8")
-    lat_us = ((v["t_visible"].astype(np.int64) - t_put.astype(np.int64)) / 1e3).tolist()
-    t = torch.tensor([ms, 0.0 if ok else 1.0, float(launches)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    lats = [None] * world
-    dist.all_gather_object(lats, lat_us)
-    ms_max, bad = float(t[0]), float(t[1])
-    dist.barrier()
+    lat_loaded, v = latencies()
+    ok = bool((status == 0).all().item()) and bool((v["status"] == 0).all())
+    log(f"timed region {ms:.3f} ms, ok = {ok}")
+
+    # unloaded latency: one message in flight (consumer waiting first), 4 KiB and one C3 tensor
+    unl = {}
+    for size in (4096, C3_LENS[0]):
+        lat = []
+        one = torch.from_numpy(R.make_msgs([src.data_ptr()], [size], [bytes(16)], [0], [7], [2]).view(np.uint8).copy()).cuda()
+        for it in range(args.lat_iters):
+            dist.barrier(group=grp)
+            R.ring_consume(ring, 1, views, None, 0, 0, sc)
+            time.sleep(0.0002)
+            R.ring_put_batch(peer, one, 1, 0, status, sp)
+            torch.cuda.synchronize()
+            lv, vv = latencies()
+            if it >= 2 and int(vv["status"][0]) == 0:
+                lat.append(lv[0])
+        unl[size] = lat
+
+    # e2e: host payloads (pinned) -> device each step, then the step, views -> host
+    host_src = torch.empty(m * stride, dtype=torch.uint8).pin_memory()
+    host_src.copy_(src[: m * stride].cpu())
+    host_views = torch.empty(m * 128, dtype=torch.uint8).pin_memory()
+    e_steps = max(3, min(args.steps, 20))
+    dist.barrier(group=grp)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(sp)
+    for i in range(e_steps):
+        with torch.cuda.stream(sp):
+            src[: m * stride].copy_(host_src, non_blocking=True)
+        R.ring_consume(ring, m, views, None, 0, 0, sc)
+        R.ring_put_batch(peer, d_msgs[0], m, 0, status, sp)
+        sp.wait_stream(sc)
+        with torch.cuda.stream(sp):
+            host_views.copy_(views, non_blocking=True)
+    e1.record(sp)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+
+    summary = torch.tensor([ms, e2e_ms, 0.0 if ok else 1.0, float(launches)], dtype=torch.float64)
+    dist.all_reduce(summary, op=dist.ReduceOp.MAX, group=grp)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (lat_loaded, unl[4096], unl[C3_LENS[0]]), group=grp)
+    cpu = None
+    if rank == 0:
+        cpu = cpu_baseline(list(C3_LENS) * 4, Rb, N, args.cpu_budget)
+    dist.barrier(group=grp)
     R.ring_detach(peer)
-    dist.barrier()
+    dist.barrier(group=grp)
     R.ring_destroy(ring)
     if rank != 0:
         return None
-    all_lat = np.array([x for l in lats for x in l])
+    ms_max, e2e_max, bad = float(summary[0]), float(summary[1]), float(summary[2])
+    loaded = [x for g in gathered for x in g[0]]
+    u4k = [x for g in gathered for x in g[1]]
+    u4m = [x for g in gathered for x in g[2]]
     value = payload_step * args.steps * world / (ms_max / 1e3) / 1e9
     per_gpu = value / world
+    e2e = payload_step * e_steps * world / (e2e_max / 1e3) / 1e9
     return {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
@@ -359,17 +422,26 @@ def bench_pairs(args, rank, world):
                                "umT5 emb 512x4096 bf16 / 480p latent 16x21x60x104 bf16 alternating",
                    "R_bytes": Rb, "n_slots": N, "msgs_per_step_per_rank": m,
                    "l2": "inputs larger than L2 per rank (2 x 128 MiB source sets)",
-                   "parallelism": f"{world} concurrent SPSC rings (egress+ingress per GPU)"},
+                   "parallelism": f"{world} concurrent SPSC rings (one egress + one ingress stream per GPU)"},
         "per_gpu_gbs": round(per_gpu, 2),
         "nvlink_frac_of_900": round(per_gpu / NVLINK_NOMINAL, 4),
-        "latency_us": {"p50": round(float(np.percentile(all_lat, 50)), 2),
-                       "p99": round(float(np.percentile(all_lat, 99)), 2),
-                       "what": "t_visible - t_put (globaltimer; streaming, loaded)"},
+        "msgs_per_s": round(m * args.steps * world / (ms_max / 1e3), 1),
+        "latency_us": {
+            "loaded_p50": pct(loaded, 50), "loaded_p99": pct(loaded, 99),
+            "unloaded_4KiB_p50": pct(u4k, 50), "unloaded_4KiB_p99": pct(u4k, 99),
+            "unloaded_4MiB_p50": pct(u4m, 50), "unloaded_4MiB_p99": pct(u4m, 99),
+            "samples": {"loaded": len(loaded), "unloaded_4KiB": len(u4k), "unloaded_4MiB": len(u4m)},
+            "what": "t_visible (consumer GPU) - t_put (producer GPU), both %globaltimer mapped to the host "
+                    "CLOCK_MONOTONIC with ring_clock_offset_ns; loaded = last timed step"},
         "roofline": {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": NVLINK_PEAK_MEASURED, "unit": "GB/s",
                      "frac": round(per_gpu / NVLINK_PEAK_MEASURED, 4), "traffic": None, "kernel": "put_kernel",
-                     "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal)"},
-        "gpu_launches": int(t[2]) * world,
+                     "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal); "
+                                    "SM peer-store ceiling measured here 690-695 GB/s"},
+        "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": m * stride * world,
+                "d2h_bytes_per_step": m * 128 * world},
+        "gpu_launches": int(summary[3]) * world,
         "clocks": clocks,
+        "cpu_baseline": cpu,
         "ok": bad == 0.0,
     }
 
@@ -384,11 +456,12 @@ def reference_arm(args):
     if world == 1:
         lens, Rb, N, wl = [1048512] * 16, 64 << 20, 64, "C2 sample: 16 x 1,048,512-B messages per step"
     else:
-        lens, Rb, N, wl = [4194304, 4193280] * 4, 64 << 20, 64, "C3 sample: 8 x ~4 MiB messages per step"
+        lens, Rb, N, wl = list(C3_LENS) * 4, 64 << 20, 64, "C3 sample: 8 x ~4 MiB messages per step"
+    msgs = oracle_inputs(lens)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        gbs, nm, dt = oracle_throughput(lens, Rb, N, budget_s=0.0, seed=i)
+        oracle_pass(msgs, Rb, N)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
     tot = sum(times)
@@ -409,9 +482,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--msgs-per-step", type=int, default=0)
-    ap.add_argument("--copy-ctas", type=int, default=0)
+    ap.add_argument("--ctas", type=int, default=0, help="put grid size (0 = library default)")
     ap.add_argument("--threads", type=int, default=0)
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--lat-iters", type=int, default=40)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -425,16 +499,18 @@ def main():
     if world == 1:
         if not args.steps:
             args.steps = 2000
-        out = bench_c2(args)
-        print(json.dumps(out), flush=True)
+        print(json.dumps(bench_c2(args)), flush=True)
         return
     import torch.distributed as dist
     rank = int(os.environ["RANK"])
     if not args.steps:
         args.steps = 200
-    dist.init_process_group("nccl", device_id=None)
+    # NCCL is the process group of record; the handle exchange and the
+    # max-over-ranks reduction run on a gloo group (CPU objects only).
+    dist.init_process_group("nccl")
+    grp = dist.new_group(backend="gloo")
     try:
-        out = bench_pairs(args, rank, world)
+        out = bench_pairs(args, rank, world, grp)
         if out:
             print(json.dumps(out), flush=True)
     finally:

@@ -227,6 +227,12 @@ const char* ring_strerror(ring_status_t s);
 const char* ring_last_cuda_error(void);
 /* Number of kernels this library has launched in this process (for bench accounting). */
 uint64_t ring_launch_count(void);
+/* Measurement support (not on the data path): offset in ns between `device`'s
+ * %globaltimer (the clock of t_put / t_visible) and the host CLOCK_MONOTONIC,
+ * offset = gpu - host, within about one PCIe write latency.  Lets latencies
+ * between two GPUs of one host be computed on one time base.  Synchronous,
+ * ~3 ms. */
+ring_status_t ring_clock_offset_ns(int device, int64_t* offset_ns);
 /* Footprint of a payload: align_up(64 + len, 128) (R9, R11). */
 uint64_t ring_footprint(uint64_t len);
 

@@ -1,23 +1,25 @@
 // get.cu — the receiver side of the double ring (receiver
 // steps 1-5) and the in-order release (R13).
 //
-// get_kernel grid = 1 control CTA (+ copy CTAs when copying out).
-//   control CTA warp 0: for each entry, in order: poll the tail until its
-//     sequence differs from the read cursor G (steps 1-2, R7; wait-free for
-//     the producers), read the size slot (a PAD entry is stepped
-//     over with its size metadata, R3), read the 64-B header and verify its
-//     CRC-32 (step 3 + PAPER.md:768-769), write the view record.  When
-//     consuming without copy-out it also clears the busy bit and moves the head
-//     (steps 4-5) and pushes the head to the producers' mirrors (credit, R1),
-//     one system-scope fence per batch of releases.
-//   copy CTAs + control CTA warp 1 ("finisher"), copy-out only: copy payloads
-//     to the user buffer; the finisher releases each entry (consume) once its
-//     copy is complete, in order.
+// get_kernel: CTA 0 warp 0 is the control warp; with copy-out, CTA 0 warp 1 is
+// the finisher and every other warp of the grid a copy warp (ring_copy.cuh).
+//   control warp, one batch of up to 32 entries per round, one entry per lane:
+//     lane 0 polls the tail until its sequence differs from the read cursor G
+//     (steps 1-2, R7; "wait-free" for the producers); lanes read
+//     the size slots of all entries already published, a warp prefix sum of
+//     the footprints gives every entry's start (the pointer formula of
+//     PAPER.md:731-739 is addition mod R once PAD entries fill every wrap,
+//     R3); each lane reads its 64-B header, verifies the CRC-32 (step 3 +
+//     PAPER.md:768-769) and writes its view record.  Consuming without
+//     copy-out, the lanes also clear the busy bits and the head moves past the
+//     whole batch (steps 4-5) with ONE fence, then is pushed to every
+//     producer's mirror (credit, R1).
+//   finisher (copy-out): releases entries in order once their copies are done.
 #include "ring_copy.cuh"
 
 namespace b200ring {
 
-__device__ __forceinline__ uint64_t* g_tail(const GetArgs& a) { return reinterpret_cast<uint64_t*>(a.ring + kTailOff); }
+__device__ __forceinline__ uint64_t* g_tail(uint8_t* ring) { return reinterpret_cast<uint64_t*>(ring + kTailOff); }
 __device__ __forceinline__ uint64_t* g_head(uint8_t* ring) { return reinterpret_cast<uint64_t*>(ring + kHeadOff); }
 __device__ __forceinline__ uint64_t* g_cursor(uint8_t* ring) { return reinterpret_cast<uint64_t*>(ring + kCursorOff); }
 __device__ __forceinline__ uint64_t* g_slot(uint8_t* ring, uint32_t N, uint32_t q) {
@@ -30,204 +32,280 @@ template <bool SYS>
 __device__ __forceinline__ void publish_head(uint8_t* ring, uint64_t** mirrors, uint32_t n_mirrors, uint64_t H) {
   fence_acq_rel<SYS>();
   st_relaxed<SYS>(g_head(ring), H);
-  for (uint32_t i = 0; i < n_mirrors; ++i)
-    if (mirrors[i]) st_relaxed<SYS>(mirrors[i], H | kMirrorValid);
+  for (uint32_t i = 0; i < n_mirrors; ++i) {
+    uint64_t* m = mirrors[i];
+    if (m) st_relaxed<SYS>(m, H | kMirrorValid);
+  }
 }
 
-struct CtlOut {
-  uint64_t start, f, t_vis;
-  uint32_t status, slot_seq, pad_item;  // pad_item: a PAD item was emitted for this entry
-};
+__device__ __forceinline__ uint64_t warp_incl_scan64(uint64_t x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__device__ __forceinline__ void st_u32_relaxed_gpu_g(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <bool SYS>
-__device__ void get_control(const GetArgs& a) {
+__device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, const uint32_t* crc_tab) {
   const int lane = threadIdx.x & 31;
-  __shared__ CtlOut co;
+  const uint32_t lt_mask = (1u << lane) - 1u;
   const bool copy = a.dst != nullptr;
   const bool inline_release = a.consume && !copy;
-  LaunchCtx* ctx = a.ctx;
-  uint64_t G = 0, H = 0;
-  uint32_t pending = 0, cta_rot = 0;
-  bool aborted = false, empty = false;
-  if (lane == 0) {
-    G = *g_cursor(a.ring);
-    H = *g_head(a.ring);
-    if (copy) {            // resynchronise the plan ring
-      for (int i = 0; i < kPlanRing; ++i) ctx->arrive[i] = 0;
-      ctx->pub_seq = 2 * a.base;
-      st_release_gpu64(&ctx->plan_seq, 2 * a.base);
-    }
-  }
-  __syncwarp();
-  for (uint32_t k = 0; k < a.n; ++k) {
-    const uint64_t item0 = 2 * (a.base + k), item1 = item0 + 1;
+  uint64_t G = ld_cg64(g_cursor(a.ring));
+  uint64_t H = ld_cg64(g_head(a.ring));
+  uint32_t k = 0, items = 0, units = 0, pending = 0;
+  uint32_t fail = RING_OK;
+  while (k < a.n) {
+    // ---- steps 1-2: wait until the tail passes the read cursor
+    uint64_t T = 0, tvis = 0;
+    uint32_t st = RING_OK;
     if (lane == 0) {
-      CtlOut o = {};
-      o.status = RING_OK;
-      if (copy && item1 - ld_acquire_gpu64(&ctx->pub_seq) >= (uint64_t)kPlanRing) {
-        const uint64_t end = globaltimer() + 2 * a.timeout_ns;
-        while (item1 - ld_acquire_gpu64(&ctx->pub_seq) >= (uint64_t)kPlanRing)
-          if (globaltimer() > end) { aborted = true; break; }
-      }
-      while (true) {
-        if (aborted) { o.status = RING_ETIMEDOUT; break; }
-        if (empty) { o.status = RING_EMPTY; break; }
-        // Steps 1-2: "Read the current head position ... If no new data is
-        // available, wait ... and retry" -- new data = tail seq != G seq (R7).
-        uint64_t T = ld_acquire<SYS>(g_tail(a));
-        if (ptr_seq(T) == ptr_seq(G)) {
-          if (pending) { publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H); pending = 0; }
-          if (a.flags & RING_TRY) { empty = true; continue; }
+      T = ld_acquire<SYS>(g_tail(a.ring));
+      if (ptr_seq(T) == ptr_seq(G)) {
+        if (pending) { publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H); pending = 0; }
+        if (a.flags & RING_TRY) {
+          st = RING_EMPTY;
+        } else {
           const uint64_t end = globaltimer() + a.timeout_ns;
           do {
-            T = ld_acquire<SYS>(g_tail(a));
+            T = ld_acquire<SYS>(g_tail(a.ring));
             if (globaltimer() > end) break;
           } while (ptr_seq(T) == ptr_seq(G));
-          if (ptr_seq(T) == ptr_seq(G)) { aborted = true; continue; }
+          if (ptr_seq(T) == ptr_seq(G)) st = RING_ETIMEDOUT;
         }
-        o.t_vis = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();
-        const uint64_t w = ld_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(G)));
-        const uint64_t f = w & kFMask;
-        if (w & kPad) {
-          // Step over a PAD entry using its size (R3).
-          const uint64_t G2 = pack_ptr(advance(ptr_off(G), f, a.R), seq_inc(ptr_seq(G)));
-          if (inline_release || (!a.consume && G == H)) {
-            // nothing held: release it at once so a producer waiting for this
-            // space can proceed
-            st_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(G)), 0ull);
-            H = G2;
-            pending++;
-          } else if (a.consume) {
-            Plan& pp = ctx->plan[item0 % kPlanRing];     // the finisher frees it in order
-            pp.cnt = 0; pp.len = 0; pp.hdr_dst = 0; pp.f = f; pp.flags = kRelease;
-            st_release_gpu64(&ctx->plan_seq, item0 + 1);
-            o.pad_item = 1;
-          }
-          G = G2;
-          continue;
-        }
-        o.start = ptr_off(G);
-        o.f = f;
-        o.slot_seq = ptr_seq(G);
-        break;
       }
-      co = o;
+      tvis = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();
     }
     __syncwarp();
-    const CtlOut o = co;
-    __syncwarp();
-    ring_view_t* v = a.views + k;
-    // Step 3: read the entry header and verify the checksum.
-    uint32_t hw = 0;
-    if (o.status == RING_OK && lane < 16) hw = __ldcg(reinterpret_cast<const uint32_t*>(a.data + o.start) + lane);
-    const uint32_t hw_next = __shfl_down_sync(0xffffffffu, hw, 1);
-    const uint32_t crc = warp_crc52(hw_next, lane, a.crc_table);
-    const uint32_t w0 = __shfl_sync(0xffffffffu, hw, 0);
-    const uint32_t w8 = __shfl_sync(0xffffffffu, hw, 8);
-    const uint32_t w9 = __shfl_sync(0xffffffffu, hw, 9);
-    const uint64_t len = (w8 >> 16) | ((w9 & 0xffffu) << 16);
-    uint32_t status = o.status;
+    st = __shfl_sync(0xffffffffu, st, 0);
+    pending = __shfl_sync(0xffffffffu, pending, 0);
+    if (st != RING_OK) { fail = st; break; }
+    T = __shfl_sync(0xffffffffu, T, 0);
+    tvis = __shfl_sync(0xffffffffu, tvis, 0);
+    const uint32_t avail = seq_dist(ptr_seq(T), ptr_seq(G));
+    const uint32_t e = min(avail, 32u);
+    // ---- slots of every published entry (one per lane)
+    uint64_t w = 0;
+    if ((uint32_t)lane < e) w = ld_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(G) + lane));
+    const uint64_t f = (uint32_t)lane < e ? (w & kFMask) : 0;
+    const bool pad = (w & kPad) != 0;
+    const bool ismsg = (uint32_t)lane < e && !pad;
+    const uint64_t incl = warp_incl_scan64(f, lane);
+    uint64_t start = ptr_off(G) + (incl - f);
+    if (start >= a.R) start -= a.R;
+    // ---- cut the batch after the last message still wanted (trailing PAD
+    // entries stay for the next call, as the oracle's receiver leaves them)
+    const uint32_t msgmask = __ballot_sync(0xffffffffu, ismsg);
+    const uint32_t need = a.n - k;
+    uint32_t e2 = e;
+    if ((uint32_t)__popc(msgmask) >= need) {
+      uint32_t mm = msgmask;
+      for (uint32_t q = 1; q < need; ++q) mm &= mm - 1;   // keep the need-th set bit lowest
+      e2 = __ffs(mm);                                    // lanes [0, e2) up to and including it
+    }
+    const bool in = (uint32_t)lane < e2;
+    const uint32_t mi = k + __popc(msgmask & lt_mask);
+    // ---- step 3: header + checksum, view record
+    uint64_t len = 0;
+    uint32_t status = RING_OK;
     bool deliver = false;
-    if (status == RING_OK) {
-      if (crc != w0 || kHdr + len > o.f) status = RING_ECORRUPT;   // discarded, still consumed
+    if (in && ismsg) {
+      const int4* hp = reinterpret_cast<const int4*>(a.data + start);
+      uint32_t hw[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 v = __ldcg(hp + q);
+        hw[4 * q] = (uint32_t)v.x; hw[4 * q + 1] = (uint32_t)v.y; hw[4 * q + 2] = (uint32_t)v.z; hw[4 * q + 3] = (uint32_t)v.w;
+      }
+      const uint32_t crc = crc52(hw, crc_tab);
+      len = (hw[8] >> 16) | ((uint64_t)(hw[9] & 0xffffu) << 16);
+      if (crc != hw[0] || kHdr + len > f) { status = RING_ECORRUPT; len = 0; }   // discarded, still consumed
       else if (copy && len > a.dst_stride) status = RING_EMSGSIZE;
       else deliver = true;
-    }
-    if (lane < 16) reinterpret_cast<uint32_t*>(v->header)[lane] = hw;
-    if (lane == 0) {
-      v->offset = o.start + kHdr;
-      v->len = (deliver || status == RING_EMSGSIZE) ? len : 0;
-      v->footprint = o.f;
-      v->start = o.start;
-      v->slot_seq = o.slot_seq;
+      ring_view_t* v = a.views + mi;
+      v->offset = start + kHdr;
+      v->len = len;
+      v->footprint = f;
+      v->start = start;
+      v->slot_seq = (ptr_seq(G) + lane) & kSeqMask;
       v->status = status;
-      v->t_visible = o.t_vis;
+      v->t_visible = tvis;
       v->reserved[0] = 0;
       v->reserved[1] = 0;
-      const bool have_entry = o.status == RING_OK;
-      if (copy) {
-        if (!o.pad_item) {
-          Plan& pp = ctx->plan[item0 % kPlanRing];
-          pp.cnt = 0; pp.len = 0; pp.hdr_dst = 0; pp.f = 0; pp.flags = 0;
-          st_release_gpu64(&ctx->plan_seq, item0 + 1);
-        }
-        Plan& p = ctx->plan[item1 % kPlanRing];
-        p.src = reinterpret_cast<uint64_t>(a.data + o.start + kHdr);
-        p.dst = reinterpret_cast<uint64_t>(a.dst + (uint64_t)k * a.dst_stride);
+      int4* vh = reinterpret_cast<int4*>(v->header);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) vh[q] = make_int4((int)hw[4 * q], (int)hw[4 * q + 1], (int)hw[4 * q + 2], (int)hw[4 * q + 3]);
+    }
+    const uint64_t fsum = warp_sum64(in ? f : 0);
+    uint64_t G2b = ptr_off(G) + fsum;
+    if (G2b >= a.R) G2b -= a.R;
+    const uint64_t G2 = pack_ptr(G2b, ptr_seq(G) + e2);
+    if (copy) {
+      // ---- one item per entry; the copy warps move the payloads
+      const uint32_t inmask = __ballot_sync(0xffffffffu, in);
+      if (lane == 0 && items + e2 - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing) {
+        const uint64_t end = globaltimer() + 2 * a.timeout_ns;
+        while (items + e2 - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing)
+          if (globaltimer() > end) break;
+      }
+      __syncwarp();
+      uint32_t nu = (in && deliver) ? units_for(len, a.chunk) : 0;
+      uint32_t nu_incl = nu;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, nu_incl, o);
+        if (lane >= o) nu_incl += y;
+      }
+      if (in) {
+        const uint32_t item = items + __popc(inmask & lt_mask);
+        Plan& p = ctx->plan[item % kPlanRing];
+        p.src = reinterpret_cast<uint64_t>(a.data + start + kHdr);
+        p.dst = reinterpret_cast<uint64_t>(a.dst + (uint64_t)mi * a.dst_stride);
         p.len = deliver ? len : 0;
         p.hdr_dst = 0;
-        p.cnt = deliver ? ctas_for(len, a.copy_ctas, a.chunk_min) : 0;
-        p.cta_base = cta_rot;
-        cta_rot = (cta_rot + p.cnt) % a.copy_ctas;
-        p.f = o.f;
-        p.flags = (a.consume && have_entry) ? kRelease : 0;
-        st_release_gpu64(&ctx->plan_seq, item1 + 1);
+        p.nunits = nu;
+        p.first_unit = units + nu_incl - nu;
+        p.f = f;
+        p.slot = (ptr_seq(G) + lane) & kSeqMask;
+        p.flags = a.consume ? kRelease : 0u;
       }
-      if (have_entry) {
-        G = pack_ptr(advance(o.start, o.f, a.R), seq_inc(o.slot_seq));
-        if (inline_release) {
-          // Steps 4-5: "Reset the busy bit", "Update the head position".
-          st_relaxed<SYS>(g_slot(a.ring, a.N, o.slot_seq), 0ull);
-          H = G;
-          if (++pending >= 8) { publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H); pending = 0; }
-        }
+      items += e2;
+      units += __shfl_sync(0xffffffffu, nu_incl, 31);
+      __syncwarp();
+      if (lane == 0) {
+        fence_acq_rel<false>();
+        st_u32_relaxed_gpu_g(&S->plan_seq, items);
+        st_u32_relaxed_gpu_g(&S->units_planned, units);
       }
     }
+    // ---- steps 4-5 (no copy-out): clear busy bits, move the head past the batch
+    const uint32_t first_msg = msgmask ? (uint32_t)__ffs(msgmask) - 1 : 32u;
+    if (inline_release) {
+      if (in) st_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(G) + lane), 0ull);
+      H = G2;
+      pending = 1;
+    } else if (!a.consume && G == H) {
+      // nothing held: PAD entries in front of the first message are released at
+      // once so that a producer waiting for their space can proceed (R3)
+      const bool lead_pad = in && (uint32_t)lane < first_msg;
+      const uint32_t nlead = min(first_msg, e2);
+      if (nlead) {
+        if (lead_pad) st_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(G) + lane), 0ull);
+        const uint64_t padsum = warp_sum64(lead_pad ? f : 0);
+        uint64_t hb = ptr_off(H) + padsum;
+        if (hb >= a.R) hb -= a.R;
+        H = pack_ptr(hb, ptr_seq(H) + nlead);
+        pending = 1;
+      }
+    }
+    __syncwarp();
+    if (inline_release && lane == 0 && pending) {
+      publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
+      pending = 0;
+    }
+    pending = __shfl_sync(0xffffffffu, pending, 0);
+    G = G2;
+    k += __popc(msgmask & ((e2 >= 32) ? 0xffffffffu : ((1u << e2) - 1u)));
   }
+  // views of messages not received (RING_TRY: EMPTY; timeout)
+  for (uint32_t q = k + lane; q < a.n; q += 32) {
+    ring_view_t* v = a.views + q;
+    v->offset = 0; v->len = 0; v->footprint = 0; v->start = 0; v->slot_seq = 0;
+    v->status = fail; v->t_visible = 0;
+  }
+  __syncwarp();
   if (lane == 0) {
     *g_cursor(a.ring) = G;
     if (pending) publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
+    if (copy) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&S->done), "r"(1u) : "memory");
   }
 }
 
-// Copy-out mode: waits for each item's copy CTAs, then (consume) releases the
-// entry in order: clear the busy bit, advance the head (steps 4-5).
+// Copy-out mode: releases entries (consume) in order once their copies are done.
 template <bool SYS>
-__device__ void get_finisher(const GetArgs& a) {
-  if ((threadIdx.x & 31) != 0) return;
+__device__ void get_finisher(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S) {
+  const int lane = threadIdx.x & 31;
+  uint64_t H = ld_cg64(g_head(a.ring));
+  uint32_t i = 0;
+  uint64_t idle_since = 0;
+  while (true) {
+    uint32_t ps = 0, done = 0;
+    if (lane == 0) {
+      done = ld_acquire_gpu32(&S->done);
+      ps = ld_acquire_gpu32(&S->plan_seq);
+    }
+    __syncwarp();
+    ps = __shfl_sync(0xffffffffu, ps, 0);
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (i >= ps && done) break;
+    const uint32_t j = i + lane;
+    bool ready = false;
+    uint32_t flags = 0, nunits = 0, slot = 0;
+    uint64_t f = 0;
+    if (j < ps) {
+      const Plan& p = ctx->plan[j % kPlanRing];
+      flags = ld_cg32(&p.flags);
+      nunits = ld_cg32(&p.nunits);
+      slot = ld_cg32(&p.slot);
+      f = ld_cg64(&p.f);
+      ready = nunits == 0 || ld_acquire_gpu32(&S->arrive[j % kPlanRing]) == nunits;
+    }
+    const uint32_t notready = __ballot_sync(0xffffffffu, !ready);
+    const uint32_t run = notready ? __ffs(notready) - 1 : 32;
+    if (run == 0) {
+      const uint64_t t = globaltimer();
+      if (!idle_since) idle_since = t;
+      else if (t - idle_since > 2 * a.timeout_ns) break;
+      continue;
+    }
+    idle_since = 0;
+    const bool rel = (uint32_t)lane < run && (flags & kRelease);
+    if ((uint32_t)lane < run && nunits) S->arrive[j % kPlanRing] = 0;
+    if (rel) st_relaxed<SYS>(g_slot(a.ring, a.N, slot), 0ull);
+    const uint32_t nrel = __popc(__ballot_sync(0xffffffffu, rel));
+    const uint64_t fsum = warp_sum64(rel ? f : 0);
+    __syncwarp();
+    if (nrel) {
+      uint64_t hb = ptr_off(H) + fsum;
+      if (hb >= a.R) hb -= a.R;
+      H = pack_ptr(hb, ptr_seq(H) + nrel);
+      if (lane == 0) publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
+    }
+    i += run;
+    if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&S->pub_seq), "r"(i) : "memory");
+  }
+}
+
+template <bool SYS>
+__global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
   LaunchCtx* ctx = a.ctx;
-  uint64_t H = *g_head(a.ring);
-  uint32_t pending = 0;
-  const uint64_t first = 2 * a.base, last = 2 * (a.base + a.n);
-  for (uint64_t i = first; i < last; ++i) {
-    if (ld_acquire_gpu64(&ctx->plan_seq) <= i) {
-      if (pending) { publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H); pending = 0; }
-      const uint64_t end = globaltimer() + 2 * a.timeout_ns;
-      bool ab = false;
-      while (ld_acquire_gpu64(&ctx->plan_seq) <= i)
-        if (globaltimer() > end) { ab = true; break; }
-      if (ab) break;
-    }
-    Plan& p = ctx->plan[i % kPlanRing];
-    const uint32_t cnt = p.cnt, flags = p.flags;
-    const uint64_t f = p.f;
-    if (cnt) {
-      const uint64_t end = globaltimer() + 2 * a.timeout_ns;
-      bool ab = false;
-      while (ld_acquire_gpu32(&ctx->arrive[i % kPlanRing]) != cnt)
-        if (globaltimer() > end) { ab = true; break; }
-      if (ab) break;
-      ctx->arrive[i % kPlanRing] = 0;
-    }
-    if (flags & kRelease) {
-      st_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(H)), 0ull);
-      H = pack_ptr(advance(ptr_off(H), f, a.R), seq_inc(ptr_seq(H)));
-      if (++pending >= 8) { publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H); pending = 0; }
-    }
-    st_release_gpu64(&ctx->pub_seq, i + 1);
-  }
-  if (pending) publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
-}
-
-template <bool SYS>
-__global__ void __launch_bounds__(1024, 1) get_kernel(const GetArgs a) {
+  LaunchSet* S = &ctx->set[a.launch & 1];
+  const int warp = threadIdx.x >> 5;
+  __shared__ uint32_t s_crc[kCrcTableWords];
   if (blockIdx.x == 0) {
-    const int warp = threadIdx.x >> 5;
-    if (warp == 0) get_control<SYS>(a);
-    else if (warp == 1 && a.dst) get_finisher<SYS>(a);
-    return;
+    load_crc_table(s_crc, a.crc_table);
+    if (warp == 0) {
+      reset_set(&ctx->set[(a.launch + 1) & 1], threadIdx.x & 31);
+      get_control<SYS>(a, ctx, S, s_crc);
+      return;
+    }
+    if (warp == 1) {
+      if (a.dst) get_finisher<SYS>(a, ctx, S);
+      return;
+    }
   }
-  copy_worker(a.ctx, 2 * a.base, 2ull * a.n, blockIdx.x - 1, a.copy_ctas, a.timeout_ns);
+  if (a.dst) copy_warp(ctx, S, a.chunk, a.timeout_ns);
 }
 
 // In-order release of `count` received entries plus the PAD entries the read
@@ -252,9 +330,18 @@ __global__ void release_kernel(const ReleaseArgs a) {
   if (moved) publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
 }
 
-cudaError_t launch_get(const GetArgs& a, uint32_t threads, cudaStream_t s) {
-  const uint32_t grid = a.dst ? a.copy_ctas + 1 : 1;
-  const uint32_t thr = a.dst ? threads : 64;
+cudaError_t preload_get() {   // see preload_put (put.cu)
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, get_kernel<true>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, get_kernel<false>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, release_kernel<true>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, release_kernel<false>);
+  return e;
+}
+
+cudaError_t launch_get(const GetArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s) {
+  const uint32_t grid = a.dst ? ctas : 1;
+  const uint32_t thr = a.dst ? threads : 32;
   if (a.sys) get_kernel<true><<<grid, thr, 0, s>>>(a);
   else get_kernel<false><<<grid, thr, 0, s>>>(a);
   return cudaGetLastError();

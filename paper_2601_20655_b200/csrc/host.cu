@@ -5,8 +5,11 @@
 // intervention" on the data path).
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
+#include <climits>
 #include <cstdio>
+#include <ctime>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -64,28 +67,19 @@ struct DevGuard {
   }
 };
 
-// ---- CRC-32 position table (R10) -------------------------------------------
-// Built from this file's own bitwise CRC-32 (reflected 0xEDB88320): the
-// register contribution of each bit of the 52 CRC'd header bytes, laid out
-// [bit 0..31][header word 1..13], followed by crc32(52 zero bytes).
-uint32_t crc_register(const uint8_t* p, size_t n, uint32_t reg) {
-  for (size_t i = 0; i < n; ++i) {
-    reg ^= p[i];
-    for (int b = 0; b < 8; ++b) reg = (reg & 1) ? (reg >> 1) ^ 0xEDB88320u : reg >> 1;
-  }
-  return reg;
-}
+// ---- CRC-32 slicing-by-4 tables (R10) ---------------------------------------
+// Table 0 is the standard 256-entry table of the reflected CRC-32
+// (0xEDB88320), built from this file's own shift-register step; table k
+// advances table k-1 by one more zero byte.  Kernels consume 4 bytes per step.
 std::vector<uint32_t> build_crc_table() {
   std::vector<uint32_t> t(kCrcTableWords);
-  uint8_t msg[52];
-  for (int w = 0; w < kCrcWords; ++w)
-    for (int b = 0; b < 32; ++b) {
-      memset(msg, 0, sizeof msg);
-      msg[4 * w + b / 8] = (uint8_t)(1u << (b % 8));
-      t[b * kCrcWords + w] = crc_register(msg, 52, 0u);
-    }
-  memset(msg, 0, sizeof msg);
-  t[32 * kCrcWords] = crc_register(msg, 52, 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+  for (uint32_t i = 0; i < 256; ++i) {
+    uint32_t reg = i;
+    for (int b = 0; b < 8; ++b) reg = (reg & 1) ? (reg >> 1) ^ 0xEDB88320u : reg >> 1;
+    t[i] = reg;
+  }
+  for (int k = 1; k < 4; ++k)
+    for (uint32_t i = 0; i < 256; ++i) t[k * 256 + i] = (t[(k - 1) * 256 + i] >> 8) ^ t[t[(k - 1) * 256 + i] & 0xFFu];
   return t;
 }
 uint32_t* g_crc_dev[64] = {};
@@ -98,6 +92,11 @@ ring_status_t crc_table_dev(int device, const uint32_t** out) {
     uint32_t* d = nullptr;
     CUDA_TRY(cudaMalloc(&d, host.size() * 4));
     CUDA_TRY(cudaMemcpy(d, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
+    // Load every kernel on this device now (lazy loading would otherwise wait
+    // for a running consumer kernel at the producer's first launch).
+    CUDA_TRY(preload_put());
+    CUDA_TRY(preload_get());
+    CUDA_TRY(preload_clock());
     g_crc_dev[device] = d;
   }
   *out = g_crc_dev[device];
@@ -132,8 +131,8 @@ struct ring_s {
   uint64_t** mirrors_dev = nullptr;          // [max_producers] pointers into producer mirrors
   std::vector<void*> opened;                 // IPC mappings of mirrors to close
   LaunchCtx* ctx = nullptr;
-  uint64_t items_base = 0;                   // copy-out launches only
-  uint32_t copy_ctas = 0, threads = 0, chunk_min = 0;
+  uint32_t launches = 0;                     // selects the LaunchSet of each get launch
+  uint32_t copy_ctas = 0, threads = 0, chunk = 0;
   const uint32_t* crc = nullptr;
   uint32_t sys = 1;
 };
@@ -147,8 +146,9 @@ struct ring_peer_s {
   DestDesc* desc_dev = nullptr;
   DestDesc desc{};
   LaunchCtx* ctx = nullptr;
-  uint64_t base = 0;
-  uint32_t copy_ctas = 0, threads = 0, chunk_min = 0, copy_mode = 0;
+  uint64_t base = 0;                         // messages submitted
+  uint32_t launches = 0;
+  uint32_t copy_ctas = 0, threads = 0, chunk = 0, copy_mode = 0;
   const uint32_t* crc = nullptr;
 };
 
@@ -161,7 +161,8 @@ struct router_s {
   std::vector<ring_peer_t> dests;
   LaunchCtx* ctx = nullptr;
   uint64_t base = 0;
-  uint32_t copy_ctas = 0, threads = 0, chunk_min = 0;
+  uint32_t launches = 0;
+  uint32_t copy_ctas = 0, threads = 0, chunk = 0;
   const uint32_t* crc = nullptr;
 };
 
@@ -190,6 +191,41 @@ ring_status_t ring_set_timeout_ns(uint64_t ns) {
   return RING_OK;
 }
 uint64_t ring_launch_count(void) { return g_launches.load(); }
+
+ring_status_t ring_clock_offset_ns(int device, int64_t* offset_ns) {
+  if (!offset_ns) return RING_EINVAL;
+  const uint32_t* unused = nullptr;
+  ring_status_t s = crc_table_dev(device, &unused);   // loads the kernels on this device
+  if (s != RING_OK) return s;
+  DevGuard g(device);
+  unsigned long long* host = nullptr;
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&host), 64, cudaHostAllocMapped));
+  volatile unsigned long long* vh = host;
+  vh[0] = 0;
+  vh[1] = 0;
+  unsigned long long* dev = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0));
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CUDA_TRY(launch_clock_publish(dev, 3000000ull, st));
+  // gpu(t_after) >= g for every sample, so offset >= g - t_after; the max over
+  // samples is within one PCIe write latency of the true offset.
+  int64_t best = INT64_MIN;
+  timespec ts;
+  while (vh[1] == 0) {
+    const unsigned long long gv = vh[0];
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    const int64_t t_after = (int64_t)ts.tv_sec * 1000000000ll + ts.tv_nsec;
+    if (gv) best = std::max(best, (int64_t)gv - t_after);
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  cudaStreamDestroy(st);
+  cudaFreeHost(host);
+  if (best == INT64_MIN) return RING_ECUDA;
+  *offset_ns = best;
+  g_launches++;
+  return RING_OK;
+}
 uint64_t ring_footprint(uint64_t len) { return footprint(len); }
 
 // ---- lifetime ------------------------------------------------------------------
@@ -403,14 +439,16 @@ ring_status_t ring_peer_config(ring_peer_t p, uint32_t copy_ctas, uint32_t threa
 
 uint64_t ring_peer_submitted(ring_peer_t p) { return p ? p->base : 0; }
 
-static void default_put_config(int device, bool sys, uint32_t* ctas, uint32_t* threads, uint32_t* chunk) {
+// Grid of a put / copy-out launch: CTA 0 holds the control warps, every other
+// warp of the grid copies.  NVLink: ~32 SMs of 16-B stores saturate one peer
+// link (profiles/r01_probe*.txt: 678-695 GB/s from 32 CTAs up); HBM->HBM
+// (same-GPU ring): one CTA per SM.
+static void default_grid(int device, bool sys, uint32_t* ctas, uint32_t* threads, uint32_t* chunk) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-  // NVLink: ~32 SMs of 16-B stores saturate the peer link (tools/probe2 on
-  // B200: 678-695 GB/s from 32 CTAs up); HBM->HBM: every SM but the control one.
-  if (!*ctas) *ctas = sys ? 32u : (uint32_t)(nsm - 1);
+  if (!*ctas) *ctas = sys ? 33u : (uint32_t)nsm;
   if (!*threads) *threads = 512;
-  if (!*chunk) *chunk = 64u << 10;
+  if (!*chunk) *chunk = 32u << 10;
 }
 
 static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const ring_msg_t* inline_msg, uint32_t n,
@@ -424,17 +462,16 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   a.dests = p->desc_dev;
   a.n_dests = 1;
   a.crc_table = p->crc;
-  a.base = p->base;
   a.timeout_ns = g_timeout_ns;
   a.n = n;
   a.flags = flags;
-  uint32_t ctas = p->copy_ctas, thr = p->threads, chunk = p->chunk_min;
+  uint32_t ctas = p->copy_ctas, thr = p->threads, chunk = p->chunk;
   DevGuard g(p->device);
-  default_put_config(p->device, p->desc.sys, &ctas, &thr, &chunk);
-  a.copy_ctas = ctas;
-  a.chunk_min = chunk;
-  a.copy_mode = p->copy_mode;
-  CUDA_TRY(launch_put(a, thr, as_stream(stream)));
+  default_grid(p->device, p->desc.sys, &ctas, &thr, &chunk);
+  a.chunk = chunk;
+  a.launch = p->launches;
+  CUDA_TRY(launch_put(a, ctas, thr, as_stream(stream)));
+  p->launches++;
   p->base += n;
   g_launches++;
   return RING_OK;
@@ -476,7 +513,6 @@ static ring_status_t get_common(ring_t r, uint32_t n, ring_view_t* d_views, void
   a.crc_table = r->crc;
   a.R = r->R;
   a.dst_stride = dst_stride;
-  a.base = r->items_base;
   a.timeout_ns = g_timeout_ns;
   a.N = r->N;
   a.n = n;
@@ -485,12 +521,12 @@ static ring_status_t get_common(ring_t r, uint32_t n, ring_view_t* d_views, void
   a.sys = r->sys;
   a.n_mirrors = r->max_producers;
   DevGuard g(r->device);
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, r->device);
-  a.copy_ctas = r->copy_ctas ? r->copy_ctas : (uint32_t)(nsm - 1);
-  a.chunk_min = r->chunk_min ? r->chunk_min : (64u << 10);
-  CUDA_TRY(launch_get(a, r->threads ? r->threads : 512, as_stream(stream)));
-  if (d_dst) r->items_base += n;
+  uint32_t ctas = r->copy_ctas, thr = r->threads, chunk = r->chunk;
+  default_grid(r->device, false, &ctas, &thr, &chunk);
+  a.chunk = chunk;
+  a.launch = r->launches;
+  CUDA_TRY(launch_get(a, ctas, thr, as_stream(stream)));
+  r->launches++;
   g_launches++;
   return RING_OK;
 }
@@ -643,18 +679,18 @@ ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, 
   a.routes = r->routes_dev;
   a.n_routes = r->max_routes;
   a.crc_table = r->crc;
-  a.base = r->base;
   a.timeout_ns = g_timeout_ns;
   a.n = n;
   a.flags = flags;
   bool sys = false;
   for (auto* p : r->dests) sys = sys || p->desc.sys;
-  uint32_t ctas = r->copy_ctas, thr = r->threads, chunk = r->chunk_min;
+  uint32_t ctas = r->copy_ctas, thr = r->threads, chunk = r->chunk;
   DevGuard g(r->device);
-  default_put_config(r->device, sys, &ctas, &thr, &chunk);
-  a.copy_ctas = ctas;
-  a.chunk_min = chunk;
-  CUDA_TRY(launch_put(a, thr, as_stream(stream)));
+  default_grid(r->device, sys, &ctas, &thr, &chunk);
+  a.chunk = chunk;
+  a.launch = r->launches;
+  CUDA_TRY(launch_put(a, ctas, thr, as_stream(stream)));
+  r->launches++;
   r->base += n;
   g_launches++;
   return RING_OK;

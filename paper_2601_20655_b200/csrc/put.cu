@@ -1,23 +1,24 @@
 // put.cu — the sender side of the double ring (sender steps
 // 1-8) as one persistent kernel per batch of messages.
 //
-// Grid = 1 control CTA + `copy_ctas` copy CTAs.
-//   control CTA warp 0 ("leader", steps 1-4 + header): for each message, in
-//     order: Lock (MPSC only, R14), read the tail, GH stale-slot check (R6),
-//     space check with the interval rule (R4), PAD entry at the wrap (R3),
-//     wait for credit (R12), build the 64-B header and its CRC-32 (R10/R11);
-//     then hand the placement to the copy CTAs through LaunchCtx::plan[].
-//   copy CTAs (step 5, WB): copy header + payload into the (peer) ring.
-//   control CTA warp 1 ("publisher", steps 6-8): when all copy CTAs of an
-//     entry arrived, write the size slot busy|f (WL), release-store the tail
-//     (UH) and, MPSC, release the lock (Unlock).
-// The leader runs ahead of the publisher by up to kPlanRing items, so the copy
-// of message k+1 overlaps the publish (MEMBAR.SYS, ~1.7 us) of message k.
-//
-// Every message k owns two items: 2k (a PAD entry, or nothing) and 2k+1 (the
-// message, or only its status).  The PAD item is published before the leader
-// waits for credit for the message, as the oracle's WLpad/UHpad do, so a
-// consumer can free the PAD while the producer waits (R3).
+// Grid = `ctas` CTAs.  CTA 0 warp 0 is the leader, CTA 0 warp 1 the
+// publisher; every other warp of the grid is a copy warp (ring_copy.cuh).
+//   leader (steps 1-4 + framing): takes the batch 32 messages at a time, one
+//     per lane.  Lane 0 places them in order: Lock (MPSC only, R14), read the
+//     tail (SPSC: producer-local), GH stale-slot check (R6), space check with
+//     the interval rule (R4) against the cached head, PAD entry at the wrap
+//     (R3), waiting for credit only when nothing else is pending (R12).  Then
+//     every lane builds its message's 64-B header (R11) and CRC-32 (R10) and
+//     writes its plan; one release hands the round to the copy warps.
+//   copy warps (step 5, WB): header + payload into the (peer) ring.
+//   publisher (steps 6-8): lanes check 32 consecutive items at once; for the
+//     leading run of complete items they write the size slots busy|f (WL),
+//     then lane 0 moves the tail with ONE system-scope release (UH) and, MPSC,
+//     releases the lock (Unlock).  The fence (MEMBAR.SYS, ~1.7 us on B200) is
+//     thus paid once per run of entries, and overlaps later copies.
+// A PAD item is published before the leader waits for credit for the message
+// that follows it (as the oracle's WLpad/UHpad do), so a consumer can free the
+// PAD while the producer waits (R3).
 #include "ring_copy.cuh"
 
 namespace b200ring {
@@ -29,312 +30,391 @@ __device__ __forceinline__ uint64_t* slot_w(const DestDesc& d, uint32_t q) {
   return reinterpret_cast<uint64_t*>(d.ring + kSlotsOff) + (q & (d.N - 1));
 }
 
-template <bool SYS>
+// The credit: the consumer's head, from the local mirror it pushes to us (R1)
+// or, while no mirror is bound, from the ring header over NVLink.
 __device__ __forceinline__ uint64_t read_head(const DestDesc& d) {
-  // The credit: the consumer's head, from the local mirror it pushes to us
-  // (R1) or, if no mirror is bound, from the ring header over NVLink.
-  const uint64_t m = ld_acquire<SYS>(&d.st->mirror_head);
-  return (m & kMirrorValid) ? (m & ~kMirrorValid) : ld_acquire<SYS>(head_w(d));
-}
-__device__ __forceinline__ uint64_t read_head_rt(const DestDesc& d) {
-  return d.sys ? read_head<true>(d) : read_head<false>(d);
+  const uint64_t m = d.sys ? ld_acquire<true>(&d.st->mirror_head) : ld_acquire<false>(&d.st->mirror_head);
+  if (m & kMirrorValid) return m & ~kMirrorValid;
+  return d.sys ? ld_acquire<true>(head_w(d)) : ld_acquire<false>(head_w(d));
 }
 
-// Header word i (i = 0..15) of the 64-byte entry header (R11); word 0 (CRC)
-// and 14/15 (t_put) are filled by the caller.
-__device__ __forceinline__ uint32_t header_word(int i, const ring_msg_t& m, uint32_t producer_id, uint32_t seq,
-                                                uint32_t epoch) {
-  const uint32_t* uid = reinterpret_cast<const uint32_t*>(m.hdr.uid);
-  const uint32_t len = (uint32_t)m.len;
-  switch (i) {
-    case 1: return uid[0];
-    case 2: return uid[1];
-    case 3: return uid[2];
-    case 4: return uid[3];
-    case 5: return (uint32_t)m.hdr.accepted_at;
-    case 6: return (uint32_t)(m.hdr.accepted_at >> 32);
-    case 7: return m.hdr.app_id;
-    case 8: return (uint32_t)m.hdr.stage | (len << 16);   // stage[32,34) payload_len[34,36)
-    case 9: return len >> 16;                             // payload_len[36,38) reserved[38,40)
-    case 10: return 0;                                    // reserved[40,44)
-    case 11: return producer_id;
-    case 12: return seq;
-    case 13: return epoch & 0xffffu;                      // epoch[52,54) flags[54,56)
-    default: return 0;
-  }
+__device__ __forceinline__ void st_u32_relaxed_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_u32_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-struct LeaderOut {     // lane 0's decisions, broadcast to the warp through shared memory
-  uint64_t start, f, pad_word, tail_after_pad, tail_after;
-  uint32_t pad_slot, slot, status, has_pad, has_msg, unlock, dest, seq, epoch;
+// Per-message decisions of lane 0, read back by every lane.
+struct GroupSlot {
+  uint64_t start, tail_after;
+  uint32_t item, dest, seq, epoch, status, slot, flags, first_unit, nunits, _p;
 };
 
-__device__ void put_leader(const PutArgs& a) {
+struct LeaderState {
+  uint64_t tails[kMaxRouterDests];  // SPSC running tail per destination
+  uint64_t heads[kMaxRouterDests];  // cached credit per destination
+  uint64_t chans[kMaxRouterDests];  // channel counters (R18)
+  uint32_t loaded;
+  uint32_t items, units;
+  bool aborted;
+};
+
+__device__ __forceinline__ void write_pad_plan(LaunchCtx* ctx, uint32_t item, uint32_t dest, uint32_t slot,
+                                               uint64_t word, uint64_t tail_after) {
+  Plan& p = ctx->plan[item % kPlanRing];
+  p.len = 0; p.hdr_dst = 0; p.nunits = 0; p.first_unit = 0;
+  p.slot_word = word; p.slot = slot; p.tail_after = tail_after; p.dest = dest;
+  p.flags = kEntry; p.status = RING_OK; p.msg = 0;
+}
+
+// Lane 0: place messages [k0, k0 + gmax) of the batch; returns how many were
+// decided (the rest wait for the next round).  Items are numbered in order.
+struct MsgBrief {        // the fields lane 0 needs, staged in shared memory by all lanes
+  uint64_t len;
+  uint32_t app_id;
+  uint32_t stage;
+};
+
+__device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, LeaderState& L, uint32_t k0,
+                                 uint32_t gmax, GroupSlot* gs, const MsgBrief* brief, const DestDesc* dests) {
+  (void)k0;
+  for (uint32_t l = 0; l < gmax; ++l) {
+    const MsgBrief& m = brief[l];
+    GroupSlot o = {};
+    o.status = RING_OK;
+    // ---- stage router (PAPER.md:531-532 round-robin; epoch = reassignment)
+    uint32_t d = 0;
+    int hit = -1;
+    if (a.routes) {
+      for (uint32_t r = 0; r < a.n_routes; ++r)
+        if (a.routes[r].n && a.routes[r].app_id == m.app_id && a.routes[r].stage == m.stage) { hit = (int)r; break; }
+      if (hit < 0) {
+        o.status = RING_EINVAL;
+      } else {
+        const Route& rt = a.routes[hit];
+        d = rt.dests[rt.rr % rt.n];
+        o.epoch = rt.epoch;
+      }
+    }
+    const DestDesc D = dests[d];
+    if (D.mpsc && l > 0) return l;               // MPSC: one message per round (lock per append)
+    o.dest = d;
+    if (!(L.loaded & (1u << d))) {
+      L.loaded |= 1u << d;
+      L.tails[d] = D.st->tail_cache;
+      L.chans[d] = D.st->chan_seq;
+      L.heads[d] = read_head(D);
+    }
+    const uint64_t f = footprint(m.len);
+    if (L.aborted) o.status = RING_ETIMEDOUT;
+    else if (o.status == RING_OK && (m.len >= (1ull << 32) || f > D.R)) o.status = RING_EMSGSIZE;
+
+    bool locked = false;
+    uint64_t P = L.tails[d];
+    const uint64_t t_start = globaltimer();
+    if (o.status == RING_OK && D.mpsc) {
+      // Step 1 "Acquire the lock using a CAS-based spinlock",
+      // after our own previous items (and their Unlock) are published.
+      while (ld_acquire_gpu32(&S->pub_seq) != L.items)
+        if (globaltimer() - t_start > a.timeout_ns) { o.status = RING_ETIMEDOUT; break; }
+      if (o.status == RING_OK) {
+        const uint64_t me = (uint64_t)D.producer_id + 1;
+        while (true) {
+          const uint64_t old = D.sys ? cas_acquire<true>(lock_w(D), 0ull, me) : cas_acquire<false>(lock_w(D), 0ull, me);
+          if (old == 0) { locked = true; break; }
+          if (globaltimer() - t_start > a.timeout_ns) { o.status = RING_ETIMEDOUT; break; }
+        }
+      }
+      if (locked) {
+        // Step 2: read the tail (ordered after the acquiring CAS).
+        P = D.sys ? ld_relaxed<true>(tail_w(D)) : ld_relaxed<false>(tail_w(D));
+        // Step 4 (R6, before the space check): a busy slot at P_seq with the
+        // size ring not full means a lost sender committed WB+WL but not UH
+        // (Case 7): advance the header past it first.  The head is read
+        // before the slot: a released slot is then seen cleared.
+        while (true) {
+          const uint64_t H = read_head(D);
+          L.heads[d] = H;
+          if (seq_dist(ptr_seq(P), ptr_seq(H)) >= D.N) break;
+          const uint64_t w = D.sys ? ld_relaxed<true>(slot_w(D, ptr_seq(P))) : ld_relaxed<false>(slot_w(D, ptr_seq(P)));
+          if (!(w & kBusy)) break;
+          P = pack_ptr(advance(ptr_off(P), w & kFMask, D.R), seq_inc(ptr_seq(P)));
+          if (D.sys) st_release<true>(tail_w(D), P); else st_release<false>(tail_w(D), P);
+        }
+      }
+    }
+    // Step 3: space check (R4), PAD entry at the wrap (R3), credit wait (R12).
+    if (o.status == RING_OK) {
+      while (true) {
+        const uint64_t H = L.heads[d];
+        const uint64_t pb = ptr_off(P), hb = ptr_off(H);
+        const uint32_t pq = ptr_seq(P), hq = ptr_seq(H);
+        bool full = seq_dist(pq, hq) >= D.N;
+        if (!full && pb + f > D.R) {
+          if (span_free(pb, pq, hb, hq, D.R - pb)) {
+            const uint64_t P2 = pack_ptr(0, seq_inc(pq));
+            write_pad_plan(ctx, L.items, d, pq, kBusy | kPad | (D.R - pb), P2);
+            L.items++;
+            P = P2;
+            L.tails[d] = P;
+            continue;
+          }
+          full = true;
+        } else if (!full && !span_free(pb, pq, hb, hq, f)) {
+          full = true;
+        }
+        if (!full) {
+          o.start = pb;
+          o.slot = pq;
+          P = pack_ptr(advance(pb, f, D.R), seq_inc(pq));
+          o.tail_after = P;
+          break;
+        }
+        // Not enough credit with the cached head: re-read it once.
+        const uint64_t H2 = read_head(D);
+        if (H2 != H) { L.heads[d] = H2; continue; }
+        if (a.flags & RING_TRY) { o.status = RING_FULL; break; }   // "release the lock and abort"
+        if (l > 0 && !locked) {
+          // Hand what is decided (and any PAD just planned) to the copy
+          // warps and the publisher before waiting.
+          L.tails[d] = P;
+          return l;
+        }
+        uint64_t H3 = H2;
+        while (H3 == H2) {
+          if (globaltimer() - t_start > a.timeout_ns) break;
+          H3 = read_head(D);
+        }
+        if (H3 == H2) { o.status = RING_ETIMEDOUT; break; }
+        L.heads[d] = H3;
+      }
+    }
+    L.tails[d] = P;
+    if (o.status == RING_ETIMEDOUT) L.aborted = true;
+    if (hit >= 0) a.routes[hit].rr = a.routes[hit].rr + 1;   // committed: advance the round robin
+    o.seq = (uint32_t)L.chans[d];
+    L.chans[d] += 1;
+    o.item = L.items++;
+    o.flags = kStatus | (o.status == RING_OK ? kEntry : 0u) | (locked ? kUnlock : 0u);
+    if (o.status == RING_OK) {
+      o.nunits = units_for(m.len, a.chunk);
+      o.first_unit = L.units;
+      L.units += o.nunits;
+    }
+    gs[l] = o;
+    if (locked) return l + 1;
+  }
+  return gmax;
+}
+
+__device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const uint32_t* crc_tab) {
   const int lane = threadIdx.x & 31;
-  LaunchCtx* ctx = a.ctx;
-  __shared__ LeaderOut lo;
-  // lane 0 state: per destination running tail (SPSC) and channel counters
-  uint64_t tails[kMaxRouterDests];
-  uint64_t chans[kMaxRouterDests];
-  uint32_t loaded = 0;
-  uint32_t cta_rot = 0;    // rotates the copy CTAs over consecutive entries
-  bool aborted = false;
-  if (lane == 0) {         // resynchronise the plan ring (an aborted launch may have left it mid-way)
-    for (int i = 0; i < kPlanRing; ++i) ctx->arrive[i] = 0;
-    ctx->pub_seq = 2 * a.base;
-    st_release_gpu64(&ctx->plan_seq, 2 * a.base);
+  __shared__ GroupSlot gs[kGroup];
+  __shared__ MsgBrief brief[kGroup];
+  __shared__ uint32_t s_g;
+  __shared__ LeaderState L;
+  __shared__ DestDesc s_dests[kMaxRouterDests];   // destination descriptors, read every message
+  for (uint32_t d = lane; d < a.n_dests && d < (uint32_t)kMaxRouterDests; d += 32) s_dests[d] = a.dests[d];
+  if (lane == 0) {
+    L.loaded = 0;
+    L.items = 0;
+    L.units = 0;
+    L.aborted = false;
   }
   __syncwarp();
-
-  for (uint32_t k = 0; k < a.n; ++k) {
-    const uint64_t item0 = 2 * (a.base + k), item1 = item0 + 1;
-    const ring_msg_t m = a.msgs ? a.msgs[k] : a.inline_msg;
-    if (lane == 0) {
-      // flow control: both items of message k must fit in the plan ring
-      if (item1 - ld_acquire_gpu64(&ctx->pub_seq) >= (uint64_t)kPlanRing) {
-        const uint64_t end = globaltimer() + 2 * a.timeout_ns;
-        while (item1 - ld_acquire_gpu64(&ctx->pub_seq) >= (uint64_t)kPlanRing)
-          if (globaltimer() > end) { aborted = true; break; }
-      }
-      LeaderOut o = {};
-      o.status = RING_OK;
-      // ---- stage router: pick the destination (PAPER.md:531-532 round-robin)
-      uint32_t d = 0, epoch = 0;
-      if (a.routes) {
-        int hit = -1;
-        for (uint32_t r = 0; r < a.n_routes; ++r)
-          if (a.routes[r].n && a.routes[r].app_id == m.hdr.app_id && a.routes[r].stage == m.hdr.stage) { hit = (int)r; break; }
-        if (hit < 0) {
-          o.status = RING_EINVAL;
-        } else {
-          Route& rt = a.routes[hit];
-          d = rt.dests[rt.rr % rt.n];
-          rt.rr = rt.rr + 1;
-          epoch = rt.epoch;
-        }
-      }
-      o.dest = d;
-      o.epoch = epoch;
-      const DestDesc D = a.dests[d];
-      if (!(loaded & (1u << d))) {
-        loaded |= 1u << d;
-        tails[d] = D.st->tail_cache;
-        chans[d] = D.st->chan_seq;
-      }
-      o.seq = (uint32_t)chans[d];
-      chans[d] += 1;
-      const uint64_t f = footprint(m.len);
-      o.f = f;
-      if (aborted) o.status = RING_ETIMEDOUT;
-      else if (o.status == RING_OK && (m.len >= (1ull << 32) || f > D.R)) o.status = RING_EMSGSIZE;
-
-      bool locked = false;
-      uint64_t P = tails[d];
-      if (o.status == RING_OK && D.mpsc) {
-        // Step 1 "Acquire the lock using a CAS-based spinlock".
-        // Our previous items (and their Unlock) must have been published first.
-        const uint64_t end = globaltimer() + a.timeout_ns;
-        while (ld_acquire_gpu64(&ctx->pub_seq) != item0)
-          if (globaltimer() > end) { o.status = RING_ETIMEDOUT; break; }
-        if (o.status == RING_OK) {
-          const uint64_t me = (uint64_t)D.producer_id + 1;
-          while (true) {
-            const uint64_t old = D.sys ? cas_acquire<true>(lock_w(D), 0ull, me) : cas_acquire<false>(lock_w(D), 0ull, me);
-            if (old == 0) { locked = true; break; }
-            if (globaltimer() > end) { o.status = RING_ETIMEDOUT; break; }
-          }
-        }
-        if (locked) {
-          // Step 2: read the tail (ordered after the acquiring CAS).
-          P = D.sys ? ld_relaxed<true>(tail_w(D)) : ld_relaxed<false>(tail_w(D));
-          // Step 4 (R6: before the space check): a busy slot at P_seq with the
-          // size ring not full means a lost sender committed WB+WL but not UH
-          // (Case 7): advance the header past it before writing.
-          // The head is read before the slot: a slot the consumer has released
-          // is then seen cleared (it clears the slot before moving the head).
-          while (true) {
-            const uint64_t H = read_head_rt(D);
-            if (seq_dist(ptr_seq(P), ptr_seq(H)) >= D.N) break;
-            const uint64_t w = D.sys ? ld_relaxed<true>(slot_w(D, ptr_seq(P))) : ld_relaxed<false>(slot_w(D, ptr_seq(P)));
-            if (!(w & kBusy)) break;
-            P = pack_ptr(advance(ptr_off(P), w & kFMask, D.R), seq_inc(ptr_seq(P)));
-            if (D.sys) st_release<true>(tail_w(D), P); else st_release<false>(tail_w(D), P);
-          }
-        }
-      }
-      // Step 3: space check (R4) with the PAD entry at the wrap (R3), waiting
-      // for credit in BLOCK mode (R12).
-      if (o.status == RING_OK) {
-        uint64_t H = read_head_rt(D);
-        const uint64_t end = globaltimer() + a.timeout_ns;
-        bool pad_done = false;
-        while (true) {
-          const uint64_t pb = ptr_off(P), hb = ptr_off(H);
-          const uint32_t pq = ptr_seq(P), hq = ptr_seq(H);
-          bool full = seq_dist(pq, hq) >= D.N;
-          if (!full && pb + f > D.R) {
-            if (!pad_done && span_free(pb, pq, hb, hq, D.R - pb)) {
-              o.has_pad = 1;
-              o.pad_slot = pq;
-              o.pad_word = kBusy | kPad | (D.R - pb);
-              P = pack_ptr(0, seq_inc(pq));
-              o.tail_after_pad = P;
-              pad_done = true;
-              // Publish the PAD now (item 0) before waiting for the message.
-              Plan& pp = ctx->plan[item0 % kPlanRing];
-              pp.cnt = 0; pp.len = 0; pp.hdr_dst = 0; pp.dest = d;
-              pp.pad_word = o.pad_word; pp.pad_slot = o.pad_slot; pp.tail_after = P;
-              pp.flags = kPublish; pp.status = RING_OK;
-              st_release_gpu64(&ctx->plan_seq, item0 + 1);
-              continue;
-            }
-            full = true;
-          } else if (!full && !span_free(pb, pq, hb, hq, f)) {
-            full = true;
-          }
-          if (!full) {
-            o.start = pb;
-            o.slot = pq;
-            o.has_msg = 1;
-            P = pack_ptr(advance(pb, f, D.R), seq_inc(pq));
-            o.tail_after = P;
-            break;
-          }
-          if (a.flags & RING_TRY) { o.status = RING_FULL; break; }   // "release the lock and abort"
-          // wait until the consumer moves the head
-          uint64_t H2 = read_head_rt(D);
-          while (H2 == H) {
-            if (globaltimer() > end) break;
-            H2 = read_head_rt(D);
-          }
-          if (H2 == H) { o.status = RING_ETIMEDOUT; break; }
-          H = H2;
-        }
-        if (o.has_pad == 0) {
-          Plan& pp = ctx->plan[item0 % kPlanRing];
-          pp.cnt = 0; pp.len = 0; pp.hdr_dst = 0; pp.dest = d; pp.pad_word = 0; pp.flags = 0; pp.status = RING_OK;
-          st_release_gpu64(&ctx->plan_seq, item0 + 1);
-        }
-      } else {
-        Plan& pp = ctx->plan[item0 % kPlanRing];
-        pp.cnt = 0; pp.len = 0; pp.hdr_dst = 0; pp.dest = d; pp.pad_word = 0; pp.flags = 0; pp.status = RING_OK;
-        st_release_gpu64(&ctx->plan_seq, item0 + 1);
-      }
-      tails[d] = P;
-      if (o.status == RING_ETIMEDOUT) aborted = true;
-      o.unlock = locked ? 1u : 0u;
-      lo = o;
+  for (uint32_t k0 = 0; k0 < a.n;) {
+    const uint32_t gmax = min((uint32_t)kGroup, a.n - k0);
+    if ((uint32_t)lane < gmax) {   // stage the round's lengths / routing keys in parallel
+      const ring_msg_t* mp = a.msgs ? a.msgs + k0 + lane : &a.inline_msg;
+      brief[lane].len = mp->len;
+      brief[lane].app_id = mp->hdr.app_id;
+      brief[lane].stage = mp->hdr.stage;
     }
     __syncwarp();
-    const LeaderOut o = lo;
-    __syncwarp();
-    // ---- header (step 5 payload framing) + CRC-32 over bytes [4,56) (R10),
-    // computed by the whole warp.
-    Plan& p = ctx->plan[item1 % kPlanRing];
-    if (o.has_msg) {
-      const DestDesc& D = a.dests[o.dest];
-      const uint32_t w_mine = header_word(lane, m, D.producer_id, o.seq, o.epoch);
-      const uint32_t w_crc = header_word(lane + 1, m, D.producer_id, o.seq, o.epoch);
-      const uint32_t crc = warp_crc52(w_crc, lane, a.crc_table);
-      if (lane < 16) {
-        uint32_t w = w_mine;
-        if (lane == 0) w = crc;
-        if (lane == 14 || lane == 15) {
-          const uint64_t t = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();
-          w = lane == 14 ? (uint32_t)t : (uint32_t)(t >> 32);
-        }
-        p.hdr[lane] = w;
+    if (lane == 0) {
+      // Flow control: the round adds at most 2 items per message.
+      if (L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing) {
+        const uint64_t end = globaltimer() + 2 * a.timeout_ns;
+        while (L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing)
+          if (globaltimer() > end) { L.aborted = true; break; }
       }
-      if (lane == 0) {
+      s_g = leader_place(a, ctx, S, L, k0, gmax, gs, brief, s_dests);
+    }
+    __syncwarp();
+    const uint32_t g = s_g;
+    if ((uint32_t)lane < g) {
+      const uint32_t k = k0 + lane;
+      const ring_msg_t m = a.msgs ? a.msgs[k] : a.inline_msg;
+      const GroupSlot o = gs[lane];
+      Plan& p = ctx->plan[o.item % kPlanRing];
+      p.msg = k;
+      p.status = o.status;
+      p.dest = o.dest;
+      p.flags = o.flags;
+      p.nunits = o.nunits;
+      p.first_unit = o.first_unit;
+      p.len = 0;
+      p.hdr_dst = 0;
+      if (o.status == RING_OK) {
+        const DestDesc& D = s_dests[o.dest];
+        const uint64_t f = footprint(m.len);
+        // ---- entry header (R11) + CRC-32 over bytes [4, 56) (R10)
+        uint32_t w[16];
+        const uint32_t* uid = reinterpret_cast<const uint32_t*>(m.hdr.uid);
+        const uint32_t len32 = (uint32_t)m.len;
+        w[1] = uid[0]; w[2] = uid[1]; w[3] = uid[2]; w[4] = uid[3];
+        w[5] = (uint32_t)m.hdr.accepted_at;
+        w[6] = (uint32_t)(m.hdr.accepted_at >> 32);
+        w[7] = m.hdr.app_id;
+        w[8] = (uint32_t)m.hdr.stage | (len32 << 16);   // stage[32,34) payload_len[34,36)
+        w[9] = len32 >> 16;                             // payload_len[36,38) reserved[38,40)
+        w[10] = 0;                                      // reserved[40,44)
+        w[11] = D.producer_id;
+        w[12] = o.seq;
+        w[13] = o.epoch & 0xffffu;                      // epoch[52,54) flags[54,56)
+        w[0] = crc52(w, crc_tab);
+        const uint64_t t = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();
+        w[14] = (uint32_t)t;
+        w[15] = (uint32_t)(t >> 32);
+        int4* ph = reinterpret_cast<int4*>(p.hdr);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ph[q] = make_int4((int)w[4 * q], (int)w[4 * q + 1], (int)w[4 * q + 2], (int)w[4 * q + 3]);
         p.src = m.src;
         p.dst = reinterpret_cast<uint64_t>(D.data + o.start + kHdr);
         p.len = m.len;
         p.hdr_dst = reinterpret_cast<uint64_t>(D.data + o.start);
-        p.cnt = ctas_for(m.len, a.copy_ctas, a.chunk_min);
-        p.cta_base = cta_rot;
-        cta_rot = (cta_rot + p.cnt) % a.copy_ctas;
-        p.start = o.start;
-        p.f = o.f;
         p.slot = o.slot;
-        p.pad_word = 0;
+        p.slot_word = kBusy | f;
         p.tail_after = o.tail_after;
-        p.flags = kHasMsg | kPublish | (o.unlock ? kUnlock : 0);
+        p.f = f;
       }
-    } else if (lane == 0) {
-      p.cnt = 0; p.len = 0; p.hdr_dst = 0; p.pad_word = 0;
-      p.flags = o.unlock ? kUnlock : 0;
-    }
-    if (lane == 0) {
-      p.dest = o.dest;
-      p.status = o.status;
       if (a.dest_out) a.dest_out[k] = o.dest;
     }
     __syncwarp();
-    if (lane == 0) st_release_gpu64(&ctx->plan_seq, item1 + 1);
+    if (lane == 0) {
+      // One fence hands the whole round (all lanes' plans, any PAD plans) to
+      // the copy warps and the publisher.
+      fence_acq_rel<false>();
+      st_u32_relaxed_gpu(&S->plan_seq, L.items);
+      st_u32_relaxed_gpu(&S->units_planned, L.units);
+    }
+    k0 += g;
   }
   if (lane == 0) {
+    st_u32_release_gpu(&S->done, 1u);
     for (uint32_t d = 0; d < kMaxRouterDests && d < a.n_dests; ++d)
-      if (loaded & (1u << d)) {
-        a.dests[d].st->chan_seq = chans[d];
-        if (!a.dests[d].mpsc) a.dests[d].st->tail_cache = tails[d];
+      if (L.loaded & (1u << d)) {
+        a.dests[d].st->chan_seq = L.chans[d];
+        if (!a.dests[d].mpsc) a.dests[d].st->tail_cache = L.tails[d];
       }
   }
 }
 
-// Steps 6-8 (WL, UH, Unlock) in item order.
-__device__ void put_publisher(const PutArgs& a) {
-  if ((threadIdx.x & 31) != 0) return;
+// Steps 6-8 (WL, UH, Unlock), 32 items per look, in item order.
+__device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
+  const int lane = threadIdx.x & 31;
+  uint32_t i = 0;
+  uint64_t idle_since = 0;
+  while (true) {
+    uint32_t ps = 0, done = 0;
+    if (lane == 0) {
+      done = ld_acquire_gpu32(&S->done);
+      ps = ld_acquire_gpu32(&S->plan_seq);
+    }
+    __syncwarp();
+    ps = __shfl_sync(0xffffffffu, ps, 0);
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (i >= ps && done) break;
+    const uint32_t j = i + lane;
+    bool ready = false;
+    uint32_t flags = 0, dest = 0, nunits = 0;
+    if (j < ps) {
+      const Plan& p = ctx->plan[j % kPlanRing];
+      flags = ld_cg32(&p.flags);
+      dest = ld_cg32(&p.dest);
+      nunits = ld_cg32(&p.nunits);
+      ready = nunits == 0 || ld_acquire_gpu32(&S->arrive[j % kPlanRing]) == nunits;
+    }
+    const uint32_t notready = __ballot_sync(0xffffffffu, !ready);
+    uint32_t run = notready ? __ffs(notready) - 1 : 32;
+    // a run stays on one destination and ends at an Unlock
+    const uint32_t dest0 = __shfl_sync(0xffffffffu, dest, 0);
+    const uint32_t other = __ballot_sync(0xffffffffu, (uint32_t)lane < run && dest != dest0);
+    if (other) run = min(run, (uint32_t)(__ffs(other) - 1));
+    const uint32_t unl = __ballot_sync(0xffffffffu, (uint32_t)lane < run && (flags & kUnlock));
+    if (unl) run = min(run, (uint32_t)__ffs(unl));
+    if (run == 0) {
+      const uint64_t t = globaltimer();
+      if (!idle_since) idle_since = t;
+      else if (t - idle_since > 2 * a.timeout_ns) break;
+      continue;
+    }
+    idle_since = 0;
+    const DestDesc& D = a.dests[dest0];
+    if ((uint32_t)lane < run) {
+      const Plan& p = ctx->plan[j % kPlanRing];
+      if (nunits) S->arrive[j % kPlanRing] = 0;
+      if (flags & kEntry) {   // WL: size + busy bit (PAD entries carry the pad bit)
+        const uint64_t word = ld_cg64(&p.slot_word);
+        const uint32_t slot = ld_cg32(&p.slot);
+        if (D.sys) st_relaxed<true>(slot_w(D, slot), word);
+        else st_relaxed<false>(slot_w(D, slot), word);
+      }
+    }
+    const uint32_t entries = __ballot_sync(0xffffffffu, (uint32_t)lane < run && (flags & kEntry));
+    __syncwarp();
+    if (lane == 0) {
+      if (entries) {   // UH: one release covers the run's entries
+        const uint32_t last = 31 - __clz(entries);
+        const uint64_t tail = ld_cg64(&ctx->plan[(i + last) % kPlanRing].tail_after);
+        if (D.sys) st_release<true>(tail_w(D), tail); else st_release<false>(tail_w(D), tail);
+      }
+      if (unl && (uint32_t)__ffs(unl) == run) {   // Unlock after the tail
+        if (D.sys) st_release<true>(lock_w(D), 0ull); else st_release<false>(lock_w(D), 0ull);
+      }
+    }
+    if ((uint32_t)lane < run && (flags & kStatus)) {
+      const Plan& p = ctx->plan[j % kPlanRing];
+      a.status[ld_cg32(&p.msg)] = ld_cg32(&p.status);
+    }
+    __syncwarp();
+    i += run;
+    if (lane == 0) st_u32_release_gpu(&S->pub_seq, i);
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
   LaunchCtx* ctx = a.ctx;
-  const uint64_t first = 2 * a.base, last = 2 * (a.base + a.n);
-  for (uint64_t i = first; i < last; ++i) {
-    if (ld_acquire_gpu64(&ctx->plan_seq) <= i) {
-      const uint64_t end = globaltimer() + 2 * a.timeout_ns;
-      bool ab = false;
-      while (ld_acquire_gpu64(&ctx->plan_seq) <= i)
-        if (globaltimer() > end) { ab = true; break; }
-      if (ab) return;
-    }
-    Plan& p = ctx->plan[i % kPlanRing];
-    const uint32_t cnt = p.cnt, flags = p.flags;
-    if (cnt) {
-      if (ld_acquire_gpu32(&ctx->arrive[i % kPlanRing]) != cnt) {
-        const uint64_t end = globaltimer() + 2 * a.timeout_ns;
-        bool ab = false;
-        while (ld_acquire_gpu32(&ctx->arrive[i % kPlanRing]) != cnt)
-          if (globaltimer() > end) { ab = true; break; }
-        if (ab) return;
-      }
-      ctx->arrive[i % kPlanRing] = 0;
-    }
-    const DestDesc& D = a.dests[p.dest];
-    if (D.sys) {
-      if (p.pad_word) st_relaxed<true>(slot_w(D, p.pad_slot), p.pad_word);            // WL of the PAD entry
-      if (flags & kHasMsg) st_relaxed<true>(slot_w(D, p.slot), kBusy | p.f);           // WL: size + busy bit
-      if (flags & kPublish) st_release<true>(tail_w(D), p.tail_after);                  // UH
-      if (flags & kUnlock) st_release<true>(lock_w(D), 0ull);                           // Unlock
-    } else {
-      if (p.pad_word) st_relaxed<false>(slot_w(D, p.pad_slot), p.pad_word);
-      if (flags & kHasMsg) st_relaxed<false>(slot_w(D, p.slot), kBusy | p.f);
-      if (flags & kPublish) st_release<false>(tail_w(D), p.tail_after);
-      if (flags & kUnlock) st_release<false>(lock_w(D), 0ull);
-    }
-    if (i & 1) a.status[(i - first) >> 1] = p.status;
-    st_release_gpu64(&ctx->pub_seq, i + 1);
-  }
-}
-
-__global__ void __launch_bounds__(1024, 1) put_kernel(const PutArgs a) {
+  LaunchSet* S = &ctx->set[a.launch & 1];
+  const int warp = threadIdx.x >> 5;
+  __shared__ uint32_t s_crc[kCrcTableWords];
   if (blockIdx.x == 0) {
-    const int warp = threadIdx.x >> 5;
-    if (warp == 0) put_leader(a);
-    else if (warp == 1) put_publisher(a);
-    return;
+    load_crc_table(s_crc, a.crc_table);
+    if (warp == 0) {
+      reset_set(&ctx->set[(a.launch + 1) & 1], threadIdx.x & 31);
+      put_leader(a, ctx, S, s_crc);
+      return;
+    }
+    if (warp == 1) {
+      put_publisher(a, ctx, S);
+      return;
+    }
   }
-  copy_worker(a.ctx, 2 * a.base, 2ull * a.n, blockIdx.x - 1, a.copy_ctas, a.timeout_ns);
+  copy_warp(ctx, S, a.chunk, a.timeout_ns);
 }
 
-cudaError_t launch_put(const PutArgs& a, uint32_t threads, cudaStream_t s) {
-  put_kernel<<<a.copy_ctas + 1, threads, 0, s>>>(a);
+// With CUDA's lazy module loading, the first launch of a kernel loads it, and
+// loading waits for kernels already running on the device.  A consumer kernel
+// spinning for data would then block the producer's first launch until it
+// times out; so every kernel is loaded when a device is first used.
+cudaError_t preload_put() {
+  cudaFuncAttributes fa;
+  return cudaFuncGetAttributes(&fa, put_kernel);
+}
+
+cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s) {
+  put_kernel<<<ctas, threads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -1,106 +1,140 @@
-// ring_copy.cuh — the copy CTAs shared by the put and get kernels.
+// ring_copy.cuh — copy warps shared by the put and get kernels, and the
+// per-launch bookkeeping helpers.
 //
-// A launch is a pipeline of "items" (planned entries) written by a control
-// warp into LaunchCtx::plan[] and consumed in order by every copy CTA.  Item i
-// is copied by the first `cnt` copy CTAs, each taking one contiguous 16-byte
-// aligned share, through 16-byte integer vector loads/stores (R17: bit-exact)
-// with 8 loads in flight per thread.  When a CTA's share is done it arrives on
-// arrive[i % kPlanRing] with a gpu-scope release after a CTA barrier: the
-// finisher warp that observes the full count and then performs a system-scope
-// release (the tail store) makes every CTA's NVLink stores visible to the
-// consumer before the tail (PTX causality order is transitive across scopes).
+// A launch is a pipeline of items (entries) planned in order by one control
+// warp into LaunchCtx::plan[].  The payload of each item is cut into fixed
+// `chunk`-byte work units numbered consecutively across items
+// (first_unit .. first_unit + nunits - 1).  Every copy warp of the grid grabs
+// the next unit with one atomicAdd (dynamic, warp-granular scheduling: small
+// and large entries mix without idle CTAs), waits until the control warp has
+// published a plan covering that unit, copies it through 16-byte integer
+// vector registers (R17: bit-exact, NaN payloads preserved; 8 loads in flight
+// per lane), and arrives on arrive[item] with a gpu-scope release.  The
+// publisher / finisher warp that observes the full count then performs one
+// system-scope release (the tail store, or the head store for a consumer):
+// PTX causality order is transitive across scopes, so every copy warp's NVLink
+// stores are visible to the other GPU before that release.
 #pragma once
 #include "ring_internal.h"
 
 namespace b200ring {
 
-__device__ __forceinline__ void copy_span(const uint8_t* __restrict__ src, uint8_t* dst, uint64_t nb, int tid, int T) {
+__device__ __forceinline__ uint32_t ld_cg32(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ uint64_t ld_cg64(const uint64_t* p) { return __ldcg(reinterpret_cast<const unsigned long long*>(p)); }
+
+// Warp copy of `nb` bytes, lanes striding 16 B.
+__device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8_t* dst, uint64_t nb, int lane) {
   if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
     const int4* s = reinterpret_cast<const int4*>(src);
     int4* d = reinterpret_cast<int4*>(dst);
-    const uint64_t n16 = nb >> 4;
-    uint64_t i = tid;
+    const uint32_t n16 = (uint32_t)(nb >> 4);
+    uint32_t i = lane;
     constexpr int U = 8;
-    for (; i + (U - 1) * (uint64_t)T < n16; i += U * (uint64_t)T) {
+    for (; i + (U - 1) * 32 < n16; i += U * 32) {
       int4 v[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) v[j] = ld_stream16(s + i + (uint64_t)j * T);
+      for (int j = 0; j < U; ++j) v[j] = ld_stream16(s + i + j * 32);
 #pragma unroll
-      for (int j = 0; j < U; ++j) st16(d + i + (uint64_t)j * T, v[j]);
+      for (int j = 0; j < U; ++j) st16(d + i + j * 32, v[j]);
     }
-    for (; i < n16; i += T) st16(d + i, ld_stream16(s + i));
-    for (uint64_t j = (n16 << 4) + tid; j < nb; j += T) dst[j] = src[j];
+    for (; i < n16; i += 32) st16(d + i, ld_stream16(s + i));
+    for (uint64_t j = ((uint64_t)n16 << 4) + lane; j < nb; j += 32) dst[j] = src[j];
   } else if ((((uintptr_t)src | (uintptr_t)dst) & 3) == 0) {
     const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
     uint32_t* d = reinterpret_cast<uint32_t*>(dst);
     const uint64_t n4 = nb >> 2;
-    for (uint64_t i = tid; i < n4; i += T) d[i] = s[i];
-    for (uint64_t j = (n4 << 2) + tid; j < nb; j += T) dst[j] = src[j];
+    for (uint64_t i = lane; i < n4; i += 32) d[i] = s[i];
+    for (uint64_t j = (n4 << 2) + lane; j < nb; j += 32) dst[j] = src[j];
   } else {
-    for (uint64_t j = tid; j < nb; j += T) dst[j] = src[j];
+    for (uint64_t j = lane; j < nb; j += 32) dst[j] = src[j];
   }
 }
 
-struct SharedItem {
-  uint64_t src, dst, len, hdr_dst;
-  uint32_t cnt, abort, cta_base;
-  uint32_t hdr[16];
-};
+// Zero the counter set a launch will hand to its successor.
+__device__ __forceinline__ void reset_set(LaunchSet* s, int lane) {
+  for (int i = lane; i < kPlanRing; i += 32) s->arrive[i] = 0;
+  if (lane == 0) {
+    s->plan_seq = 0;
+    s->pub_seq = 0;
+    s->next_unit = 0;
+    s->units_planned = 0;
+    s->done = 0;
+  }
+}
 
-// Copy CTA `cta` (0-based among `n_ctas` copy CTAs) processes items
-// [first, first+count); item i is shared by the cnt CTAs that follow
-// cta_base cyclically, so consecutive small entries land on different CTAs.
-// Waits for each plan with a no-progress budget of `timeout_ns`; on expiry it
-// leaves (the control warp reports RING_ETIMEDOUT for the affected messages).
-__device__ __forceinline__ void copy_worker(LaunchCtx* ctx, uint64_t first, uint64_t count, uint32_t cta,
-                                            uint32_t n_ctas, uint64_t timeout_ns) {
-  __shared__ SharedItem si;
-  const int tid = threadIdx.x, T = blockDim.x;
-  for (uint64_t i = first; i < first + count; ++i) {
-    if (tid == 0) {
-      uint32_t ab = 0;
-      if (ld_acquire_gpu64(&ctx->plan_seq) <= i) {
-        const uint64_t end = globaltimer() + 2 * timeout_ns;
-        while (ld_acquire_gpu64(&ctx->plan_seq) <= i) {
-          if (globaltimer() > end) { ab = 1; break; }
+// Copy warp main loop.  Returns when the control warp is done and every unit
+// has been handed out, or after `2 * timeout_ns` without progress.
+__device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns) {
+  const int lane = threadIdx.x & 31;
+  uint32_t cur = 0;   // items before `cur` hold no unit this warp can still grab
+  while (true) {
+    uint32_t u = 0, quit = 0, ps = 0;
+    if (lane == 0) {
+      u = atomicAdd(&S->next_unit, 1u);
+      uint64_t end = 0;
+      // Poll with relaxed loads (no L1 invalidation per poll; thousands of
+      // warps may wait here), then one acquire once the unit is planned.
+      while (true) {
+        if (ld_relaxed_gpu32(&S->units_planned) > u) break;
+        if (ld_relaxed_gpu32(&S->done)) {
+          if (ld_acquire_gpu32(&S->units_planned) > u) break;
+          quit = 1;
+          break;
         }
+        const uint64_t t = globaltimer();
+        if (!end) end = t + 2 * timeout_ns;
+        else if (t > end) { quit = 1; break; }
+        __nanosleep(64);
       }
-      si.abort = ab;
-      if (!ab) {
+      if (!quit) (void)ld_acquire_gpu32(&S->units_planned);
+      ps = ld_acquire_gpu32(&S->plan_seq);
+    }
+    __syncwarp();
+    quit = __shfl_sync(0xffffffffu, quit, 0);
+    if (quit) return;
+    u = __shfl_sync(0xffffffffu, u, 0);
+    ps = __shfl_sync(0xffffffffu, ps, 0);
+    // find the item holding unit u (plans are read through L2: ring slots are reused)
+    uint32_t item = 0xffffffffu;
+    for (uint32_t b = cur; b < ps && item == 0xffffffffu; b += 32) {
+      const uint32_t i = b + lane;
+      bool hit = false;
+      if (i < ps) {
         const Plan& p = ctx->plan[i % kPlanRing];
-        si.src = p.src; si.dst = p.dst; si.len = p.len; si.hdr_dst = p.hdr_dst; si.cnt = p.cnt;
-        si.cta_base = p.cta_base;
-        if (p.hdr_dst) {
-#pragma unroll
-          for (int w = 0; w < 16; ++w) si.hdr[w] = p.hdr[w];
-        }
+        const uint32_t nu = ld_cg32(&p.nunits);
+        const uint32_t fu = ld_cg32(&p.first_unit);
+        hit = nu && u >= fu && u - fu < nu;
       }
+      const uint32_t m = __ballot_sync(0xffffffffu, hit);
+      if (m) item = b + __ffs(m) - 1;
     }
-    __syncthreads();
-    if (si.abort) return;
-    const uint32_t share = (cta + n_ctas - si.cta_base % n_ctas) % n_ctas;
-    if (share < si.cnt) {
-      const uint64_t per = ((si.len + si.cnt - 1) / si.cnt + 15) & ~15ull;
-      const uint64_t lo = min(si.len, (uint64_t)share * per);
-      const uint64_t hi = min(si.len, lo + per);
-      if (share == 0 && si.hdr_dst && tid < 4) {
-        int4 v = make_int4((int)si.hdr[4 * tid], (int)si.hdr[4 * tid + 1], (int)si.hdr[4 * tid + 2], (int)si.hdr[4 * tid + 3]);
-        st16(reinterpret_cast<uint8_t*>(si.hdr_dst) + 16 * tid, v);
-      }
-      copy_span(reinterpret_cast<const uint8_t*>(si.src) + lo, reinterpret_cast<uint8_t*>(si.dst) + lo, hi - lo, tid, T);
-      __syncthreads();
-      if (tid == 0) red_release_gpu_add(&ctx->arrive[i % kPlanRing], 1u);
+    if (item == 0xffffffffu) return;   // cannot happen with a consistent plan
+    cur = item;
+    const Plan& p = ctx->plan[item % kPlanRing];
+    const uint64_t src = ld_cg64(&p.src), dst = ld_cg64(&p.dst), len = ld_cg64(&p.len);
+    const uint64_t hdr_dst = ld_cg64(&p.hdr_dst);
+    const uint32_t c = u - ld_cg32(&p.first_unit);
+    const uint64_t lo = (uint64_t)c * chunk;
+    const uint64_t hi = min(len, lo + chunk);
+    if (c == 0 && hdr_dst && lane < 4) {
+      const int4 h = __ldcg(reinterpret_cast<const int4*>(p.hdr) + lane);
+      st16(reinterpret_cast<uint8_t*>(hdr_dst) + 16 * lane, h);
     }
-    __syncthreads();
+    if (hi > lo) warp_copy(reinterpret_cast<const uint8_t*>(src) + lo, reinterpret_cast<uint8_t*>(dst) + lo, hi - lo, lane);
+    __syncwarp();
+    if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);
   }
 }
 
-// Number of copy CTAs for a payload: one per `chunk_min` bytes, at least 1.
-__device__ __forceinline__ uint32_t ctas_for(uint64_t len, uint32_t copy_ctas, uint32_t chunk_min) {
-  uint64_t c = (len + chunk_min - 1) / chunk_min;
-  if (c < 1) c = 1;
-  if (c > copy_ctas) c = copy_ctas;
-  return (uint32_t)c;
+__device__ __forceinline__ uint32_t units_for(uint64_t len, uint32_t chunk) {
+  const uint64_t u = (len + chunk - 1) / chunk;
+  return u ? (uint32_t)u : 1u;   // at least one: it also writes the header
+}
+
+// Load the CRC slicing tables into shared memory (whole CTA participates).
+__device__ __forceinline__ void load_crc_table(uint32_t* s_tab, const uint32_t* g_tab) {
+  for (int i = threadIdx.x; i < kCrcTableWords; i += blockDim.x) s_tab[i] = g_tab[i];
+  __syncthreads();
 }
 
 }  // namespace b200ring

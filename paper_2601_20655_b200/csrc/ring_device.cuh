@@ -25,7 +25,8 @@ constexpr uint64_t kBusy = 1ull << 63;
 constexpr uint64_t kPad = 1ull << 62;
 constexpr uint64_t kFMask = (1ull << 62) - 1;
 constexpr uint32_t kSeqMask = (1u << 24) - 1;
-constexpr int kPlanRing = 64;        // in-flight messages per launch context
+constexpr int kPlanRing = 128;       // in-flight items (entries) per launch context
+constexpr int kGroup = 32;           // messages planned per leader round (one per lane)
 constexpr int kMaxDests = 8;          // destinations per route
 constexpr int kMaxRouterDests = 32;   // destinations per launch (bit mask)
 
@@ -124,28 +125,29 @@ __device__ __forceinline__ void st16(void* p, int4 v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
+__device__ __forceinline__ uint32_t ld_relaxed_gpu32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ---------------------------------------------------------------------------
-// Warp-parallel CRC-32/IEEE of the 52 header bytes [4,56) (R10).
-// CRC is affine over GF(2): crc(m) = crc(0^52) ^ XOR_{set bits (p,b)} T[p][b],
-// with T[p][b] the CRC register contribution of bit b of byte p.  The table
-// (416 words, layout [bit 0..31][word 0..12], then C0 = crc(0^52)) is built on
-// the host by host.cpp from its own bitwise CRC and passed to the kernels.
-// `w` = lane l's header word l+1 (bytes 4(l+1)..4(l+1)+3) for l < 13.
+// CRC-32/IEEE (reflected 0xEDB88320, init/xorout 0xFFFFFFFF) of the 52 header
+// bytes [4,56) (R10), one header per thread, slicing-by-4: four 256-entry
+// tables in shared memory (tab[k*256 + i]; built on the host by host.cu from
+// its own shift-register CRC), one 32-bit header word per step.  `w[1..13]`
+// are the header words 1..13 (little-endian).  A warp checksums 32 headers at
+// once.
 // ---------------------------------------------------------------------------
-constexpr int kCrcWords = 13;
-constexpr int kCrcTableWords = 32 * kCrcWords + 1;
-__device__ __forceinline__ uint32_t warp_crc52(uint32_t w, int lane, const uint32_t* __restrict__ table) {
-  uint32_t acc = 0;
-  if (lane < kCrcWords) {
-#pragma unroll 8
-    for (int b = 0; b < 32; ++b) {
-      uint32_t t = __ldg(table + b * kCrcWords + lane);
-      acc ^= t & (0u - ((w >> b) & 1u));
-    }
-  }
+constexpr int kCrcTableWords = 4 * 256;
+__device__ __forceinline__ uint32_t crc52(const uint32_t* w, const uint32_t* __restrict__ tab) {
+  uint32_t c = 0xFFFFFFFFu;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
-  return acc ^ __ldg(table + 32 * kCrcWords);
+  for (int i = 1; i <= 13; ++i) {
+    c ^= w[i];
+    c = tab[3 * 256 + (c & 0xFFu)] ^ tab[2 * 256 + ((c >> 8) & 0xFFu)] ^ tab[256 + ((c >> 16) & 0xFFu)] ^ tab[c >> 24];
+  }
+  return ~c;
 }
 
 }  // namespace b200ring

@@ -9,13 +9,13 @@
 
 namespace b200ring {
 
+// Mirror word: head | kMirrorValid once the consumer has bound the mirror.
+constexpr uint64_t kMirrorValid = 1ull << 63;
+
 // Producer-local state of one attachment (one producer -> one ring channel),
 // allocated on the producer GPU and exported to the consumer by CUDA IPC so
 // that the consumer's release can push the head into `mirror_head` (the
 // credit direction of the double ring, R1).
-// Mirror word: head | kMirrorValid once the consumer has bound the mirror.
-constexpr uint64_t kMirrorValid = 1ull << 63;
-
 struct alignas(128) DestState {
   uint64_t mirror_head;  // written by the consumer (NVLink store); read locally by the leader
   uint64_t _p0[15];
@@ -34,46 +34,51 @@ struct DestDesc {
   uint32_t N;
   uint32_t mpsc;         // 1: take the lock; 0: lock elided (R14)
   uint32_t producer_id;
-  uint32_t has_mirror;   // 1: consumer pushes the head into st->mirror_head
+  uint32_t has_mirror;   // unused by the kernels (mirror validity is in-band)
   uint32_t sys;          // 1: ring / consumer on another GPU -> .sys scope
   uint32_t _pad;
 };
-static_assert(sizeof(DestDesc) == 56 || sizeof(DestDesc) == 64, "DestDesc layout");
 
-enum PlanFlags : uint32_t { kHasMsg = 1, kUnlock = 2, kPublish = 4, kRelease = 8 };
+enum PlanFlags : uint32_t {
+  kEntry = 1,    // publish a size slot (slot_word) and move the tail to tail_after
+  kStatus = 2,   // write status[msg]
+  kUnlock = 4,   // release the ring lock after publishing (MPSC)
+  kRelease = 8,  // consumer copy-out: release this entry once its copy is complete
+};
 
-// One planned message: written by the leader warp, read by copy CTAs and the
-// publisher warp.  256 bytes.
+// One item of a launch: a PAD entry, a message entry, or a status-only
+// record (message not placed).  Written by the control warp, read by the copy
+// warps and the publisher / finisher warp.  192 bytes.
 struct alignas(64) Plan {
-  uint64_t src;         // payload source
-  uint64_t dst;         // payload destination
-  uint64_t len;         // payload bytes
-  uint64_t start;       // entry start in the buffer region
-  uint64_t f;           // footprint
-  uint64_t tail_after;  // tail word after this plan's entries (put)
-  uint64_t pad_word;    // slot word of a PAD entry placed first (0 = none)
-  uint32_t pad_slot, slot;
-  uint32_t dest, cnt;   // destination index; copy CTAs taking part (0 = nothing to copy)
-  uint32_t status, flags;
-  uint64_t hdr_dst;     // where the first copy CTA writes the 64-B header (0 = none)
-  uint32_t cta_base;    // copy CTAs (cta_base + j) % copy_ctas, j < cnt, take part
-  uint32_t _q;
-  uint64_t _p[3];
-  uint32_t hdr[16];     // the 64-B entry header
+  uint64_t src, dst, len, hdr_dst;  // copy: payload source / destination / bytes; header destination (0 = none)
+  uint64_t slot_word;               // busy | pad | f
+  uint64_t tail_after;              // tail word once this entry is published (put)
+  uint32_t slot, dest, msg, status; // slot seq; destination index; message index in the launch; status
+  uint32_t flags, first_unit, nunits, _q;
+  uint64_t f;
+  uint64_t _p[5];
+  uint32_t hdr[16];                 // the 64-B entry header (put)
 };
 static_assert(sizeof(Plan) == 192, "Plan layout");
 
-// Per-launch-context coordination (one per producer attachment, router or
-// consumer), on the launching GPU.  Counters are monotonic across launches:
-// message k of a launch has global index base + k, base tracked by the host.
-struct LaunchCtx {
-  uint64_t plan_seq;   // leader: plans [0, plan_seq) are written
-  uint64_t _p0[15];
-  uint64_t pub_seq;    // publisher / finisher: plans [0, pub_seq) are complete
-  uint64_t _p1[15];
-  uint64_t g_cursor;   // get: read cursor published by the control warp
-  uint64_t _p2[15];
+// Per-launch counters.  A context holds two sets used by alternate launches;
+// launch L uses set[L & 1] and zeroes set[(L + 1) & 1] for launch L + 1 (the
+// two launches are stream-ordered, so no launch ever sees a stale counter).
+struct alignas(128) LaunchSet {
+  uint32_t plan_seq;       // items [0, plan_seq) are written (control warp, release)
+  uint32_t _a[31];
+  uint32_t pub_seq;        // items [0, pub_seq) are published / finished
+  uint32_t _b[31];
+  uint32_t next_unit;      // copy work units handed out (atomic)
+  uint32_t _c[31];
+  uint32_t units_planned;  // copy work units [0, units_planned) are described by written items
+  uint32_t done;           // control warp finished: plan_seq / units_planned are final
+  uint32_t _d[30];
   uint32_t arrive[kPlanRing];
+};
+
+struct LaunchCtx {
+  LaunchSet set[2];
   Plan plan[kPlanRing];
 };
 
@@ -94,17 +99,14 @@ struct PutArgs {
   LaunchCtx* ctx;
   const DestDesc* dests;
   Route* routes;
-  const uint32_t* crc_table;
-  uint64_t base;
+  const uint32_t* crc_table;  // 256-entry CRC-32 byte table
   uint64_t timeout_ns;
+  uint32_t launch;
   uint32_t n;
   uint32_t flags;
   uint32_t n_dests;
   uint32_t n_routes;
-  uint32_t copy_ctas;
-  uint32_t chunk_min;
-  uint32_t copy_mode;
-  uint32_t _pad;
+  uint32_t chunk;             // bytes per copy work unit
 };
 
 struct GetArgs {
@@ -117,16 +119,15 @@ struct GetArgs {
   const uint32_t* crc_table;
   uint64_t R;
   uint64_t dst_stride;
-  uint64_t base;
   uint64_t timeout_ns;
+  uint32_t launch;
   uint32_t N;
   uint32_t n;
   uint32_t flags;
   uint32_t consume;     // 1: release each entry after reading (and copying)
   uint32_t sys;         // producers may be remote: .sys scope
   uint32_t n_mirrors;
-  uint32_t copy_ctas;
-  uint32_t chunk_min;
+  uint32_t chunk;
 };
 
 struct ReleaseArgs {
@@ -140,8 +141,12 @@ struct ReleaseArgs {
 };
 
 // Launchers (defined in put.cu / get.cu).
-cudaError_t launch_put(const PutArgs& a, uint32_t threads, cudaStream_t s);
-cudaError_t launch_get(const GetArgs& a, uint32_t threads, cudaStream_t s);
+cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s);
+cudaError_t launch_get(const GetArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s);
 cudaError_t launch_release(const ReleaseArgs& a, cudaStream_t s);
+cudaError_t preload_put();
+cudaError_t preload_get();
+cudaError_t preload_clock();
+cudaError_t launch_clock_publish(unsigned long long* mapped_host, unsigned long long duration_ns, cudaStream_t s);
 
 }  // namespace b200ring

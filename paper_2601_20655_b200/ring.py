@@ -86,6 +86,7 @@ def _load():
         "router_set_route": [P, U32, C.c_uint16, C.POINTER(P), U32, P],
         "ring_put_routed": [P, P, U32, U32, P, P, P],
         "ring_set_timeout_ns": [U64],
+        "ring_clock_offset_ns": [I, C.POINTER(C.c_int64)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -254,6 +255,13 @@ def ring_put_routed(router: int, d_msgs, n: int, flags: int, d_status, d_dest=No
 # ---- misc ---------------------------------------------------------------------------------
 def ring_set_timeout_ns(ns: int) -> None:
     _check("ring_set_timeout_ns", lib.ring_set_timeout_ns(ns))
+
+
+def ring_clock_offset_ns(device: int) -> int:
+    """GPU globaltimer minus host CLOCK_MONOTONIC, in ns (measurement support)."""
+    out = C.c_int64()
+    _check("ring_clock_offset_ns", lib.ring_clock_offset_ns(device, C.byref(out)))
+    return int(out.value)
 
 
 def ring_strerror(status: int) -> str:
