@@ -183,11 +183,7 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
       items += e2;
       units += __shfl_sync(0xffffffffu, nu_incl, 31);
       __syncwarp();
-      if (lane == 0) {
-        fence_acq_rel<false>();
-        st_u32_relaxed_gpu_g(&S->plan_seq, items);
-        st_u32_relaxed_gpu_g(&S->units_planned, units);
-      }
+      if (lane == 0) st_release<false>(&S->planned, make_planned(items, units));
     }
     // ---- steps 4-5 (no copy-out): clear busy bits, move the head past the batch
     const uint32_t first_msg = msgmask ? (uint32_t)__ffs(msgmask) - 1 : 32u;
@@ -242,8 +238,8 @@ __device__ void get_finisher(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   while (true) {
     uint32_t ps = 0, done = 0;
     if (lane == 0) {
-      done = ld_acquire_gpu32(&S->done);
-      ps = ld_acquire_gpu32(&S->plan_seq);
+      done = ld_acquire_gpu32(&S->done);   // before `planned`: final once done is seen
+      ps = planned_items(ld_acquire<false>(&S->planned));
     }
     __syncwarp();
     ps = __shfl_sync(0xffffffffu, ps, 0);

@@ -181,6 +181,9 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
           L.tails[d] = P;
           return l;
         }
+        // A PAD planned in this round must be published before waiting: the
+        // consumer may have to free it for this message to fit (R3).
+        st_release<false>(&S->planned, make_planned(L.items, L.units));
         uint64_t H3 = H2;
         while (H3 == H2) {
           if (globaltimer() - t_start > a.timeout_ns) break;
@@ -293,11 +296,9 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
     }
     __syncwarp();
     if (lane == 0) {
-      // One fence hands the whole round (all lanes' plans, any PAD plans) to
-      // the copy warps and the publisher.
-      fence_acq_rel<false>();
-      st_u32_relaxed_gpu(&S->plan_seq, L.items);
-      st_u32_relaxed_gpu(&S->units_planned, L.units);
+      // One release hands the whole round (all lanes' plans, any PAD plans)
+      // to the copy warps and the publisher.
+      st_release<false>(&S->planned, make_planned(L.items, L.units));
     }
     k0 += g;
   }
@@ -319,8 +320,8 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   while (true) {
     uint32_t ps = 0, done = 0;
     if (lane == 0) {
-      done = ld_acquire_gpu32(&S->done);
-      ps = ld_acquire_gpu32(&S->plan_seq);
+      done = ld_acquire_gpu32(&S->done);   // before `planned`: final once done is seen
+      ps = planned_items(ld_acquire<false>(&S->planned));
     }
     __syncwarp();
     ps = __shfl_sync(0xffffffffu, ps, 0);

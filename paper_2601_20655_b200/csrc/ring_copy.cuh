@@ -54,10 +54,9 @@ __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8
 __device__ __forceinline__ void reset_set(LaunchSet* s, int lane) {
   for (int i = lane; i < kPlanRing; i += 32) s->arrive[i] = 0;
   if (lane == 0) {
-    s->plan_seq = 0;
+    s->planned = 0;
     s->pub_seq = 0;
     s->next_unit = 0;
-    s->units_planned = 0;
     s->done = 0;
   }
 }
@@ -75,9 +74,10 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t
       // Poll with relaxed loads (no L1 invalidation per poll; thousands of
       // warps may wait here), then one acquire once the unit is planned.
       while (true) {
-        if (ld_relaxed_gpu32(&S->units_planned) > u) break;
+        if (planned_units(ld_relaxed<false>(&S->planned)) > u) break;
         if (ld_relaxed_gpu32(&S->done)) {
-          if (ld_acquire_gpu32(&S->units_planned) > u) break;
+          (void)ld_acquire_gpu32(&S->done);     // `planned` is final once done is seen
+          if (planned_units(ld_acquire<false>(&S->planned)) > u) break;
           quit = 1;
           break;
         }
@@ -86,8 +86,8 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t
         else if (t > end) { quit = 1; break; }
         __nanosleep(64);
       }
-      if (!quit) (void)ld_acquire_gpu32(&S->units_planned);
-      ps = ld_acquire_gpu32(&S->plan_seq);
+      // one acquire of the word that covered u: its items include u's item
+      ps = planned_items(ld_acquire<false>(&S->planned));
     }
     __syncwarp();
     quit = __shfl_sync(0xffffffffu, quit, 0);

@@ -65,17 +65,25 @@ static_assert(sizeof(Plan) == 192, "Plan layout");
 // launch L uses set[L & 1] and zeroes set[(L + 1) & 1] for launch L + 1 (the
 // two launches are stream-ordered, so no launch ever sees a stale counter).
 struct alignas(128) LaunchSet {
-  uint32_t plan_seq;       // items [0, plan_seq) are written (control warp, release)
-  uint32_t _a[31];
+  // (units << 32) | items, one word written with ONE release store by the
+  // control warp: items [0, items) are written and copy work units
+  // [0, units) are described by them.  (Two separate words written after one
+  // fence may become visible in either order.)
+  uint64_t planned;
+  uint64_t _a[15];
   uint32_t pub_seq;        // items [0, pub_seq) are published / finished
   uint32_t _b[31];
   uint32_t next_unit;      // copy work units handed out (atomic)
   uint32_t _c[31];
-  uint32_t units_planned;  // copy work units [0, units_planned) are described by written items
-  uint32_t done;           // control warp finished: plan_seq / units_planned are final
-  uint32_t _d[30];
+  uint32_t done;           // control warp finished: `planned` is final (release)
+  uint32_t _d[31];
   uint32_t arrive[kPlanRing];
 };
+__host__ __device__ inline uint32_t planned_items(uint64_t p) { return (uint32_t)p; }
+__host__ __device__ inline uint32_t planned_units(uint64_t p) { return (uint32_t)(p >> 32); }
+__host__ __device__ inline uint64_t make_planned(uint32_t items, uint32_t units) {
+  return ((uint64_t)units << 32) | items;
+}
 
 struct LaunchCtx {
   LaunchSet set[2];
