@@ -203,6 +203,10 @@ ring_status_t ring_read_image(ring_t ring, uint64_t* lock, uint64_t* tail, uint6
 /* Copy `len` bytes at `offset` of the buffer region to / from host memory
  * (synchronous; tests: ring-image comparison and corruption injection). */
 ring_status_t ring_read_data(ring_t ring, uint64_t offset, uint64_t len, void* host_dst);
+/* Debug: with B200RING_TRACE=1 in the environment, each put launch records a
+ * %globaltimer timeline of its leader rounds and publisher runs; copy the last
+ * one (up to n words) to host memory.  RING_EINVAL if tracing is off. */
+ring_status_t ring_peer_trace(ring_peer_t peer, uint64_t* host_out, uint32_t n);
 ring_status_t ring_write_data(ring_t ring, uint64_t offset, uint64_t len, const void* host_src);
 
 /* ---- stage router (PAPER.md:524-532 round-robin ResultDeliver; PAPER.md:914-924

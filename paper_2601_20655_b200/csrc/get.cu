@@ -38,20 +38,6 @@ __device__ __forceinline__ void publish_head(uint8_t* ring, uint64_t** mirrors, 
   }
 }
 
-__device__ __forceinline__ uint64_t warp_incl_scan64(uint64_t x, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  return x;
-}
-__device__ __forceinline__ uint64_t warp_sum64(uint64_t x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-
 __device__ __forceinline__ void st_u32_relaxed_gpu_g(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <ctime>
 #include <cstring>
 #include <mutex>
@@ -120,6 +121,8 @@ ring_status_t enable_peer(int from, int to) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+constexpr uint32_t kTraceWords = 1280;   // debug timeline of one put launch
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -149,6 +152,7 @@ struct ring_peer_s {
   uint64_t base = 0;                         // messages submitted
   uint32_t launches = 0;
   uint32_t copy_ctas = 0, threads = 0, chunk = 0, copy_mode = 0;
+  uint64_t* trace = nullptr;                 // debug timeline (B200RING_TRACE=1)
   const uint32_t* crc = nullptr;
 };
 
@@ -439,6 +443,15 @@ ring_status_t ring_peer_config(ring_peer_t p, uint32_t copy_ctas, uint32_t threa
 
 uint64_t ring_peer_submitted(ring_peer_t p) { return p ? p->base : 0; }
 
+ring_status_t ring_peer_trace(ring_peer_t p, uint64_t* host_out, uint32_t n) {
+  if (!p || !host_out) return RING_EINVAL;
+  if (!p->trace) return RING_EINVAL;
+  DevGuard g(p->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(host_out, p->trace, 8ull * std::min<uint32_t>(n, kTraceWords), cudaMemcpyDeviceToHost));
+  return RING_OK;
+}
+
 // Grid of a put / copy-out launch: CTA 0 holds the control warps, every other
 // warp of the grid copies.  NVLink: ~32 SMs of 16-B stores saturate one peer
 // link (profiles/r01_probe*.txt: 678-695 GB/s from 32 CTAs up); HBM->HBM
@@ -470,6 +483,11 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   default_grid(p->device, p->desc.sys, &ctas, &thr, &chunk);
   a.chunk = chunk;
   a.launch = p->launches;
+  if (getenv("B200RING_TRACE")) {
+    if (!p->trace) CUDA_TRY(cudaMalloc(&p->trace, kTraceWords * 8));
+    CUDA_TRY(cudaMemsetAsync(p->trace, 0, kTraceWords * 8, as_stream(stream)));
+    a.trace = p->trace;
+  }
   CUDA_TRY(launch_put(a, ctas, thr, as_stream(stream)));
   p->launches++;
   p->base += n;

@@ -70,16 +70,20 @@ __device__ __forceinline__ void write_pad_plan(LaunchCtx* ctx, uint32_t item, ui
 
 // Lane 0: place messages [k0, k0 + gmax) of the batch; returns how many were
 // decided (the rest wait for the next round).  Items are numbered in order.
-struct MsgBrief {        // the fields lane 0 needs, staged in shared memory by all lanes
+struct MsgBrief {        // the fields lane 0 needs, computed in parallel by all lanes
   uint64_t len;
+  uint64_t f;            // footprint (R9)
   uint32_t app_id;
   uint32_t stage;
+  uint32_t nunits;       // copy work units
+  uint32_t _p;
 };
 
 __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, LeaderState& L, uint32_t k0,
                                  uint32_t gmax, GroupSlot* gs, const MsgBrief* brief, const DestDesc* dests) {
   (void)k0;
   for (uint32_t l = 0; l < gmax; ++l) {
+    if (a.trace && k0 == 0 && l < 32) a.trace[128 + l] = globaltimer();
     const MsgBrief& m = brief[l];
     GroupSlot o = {};
     o.status = RING_OK;
@@ -106,13 +110,15 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
       L.chans[d] = D.st->chan_seq;
       L.heads[d] = read_head(D);
     }
-    const uint64_t f = footprint(m.len);
+    const uint64_t f = m.f;
     if (L.aborted) o.status = RING_ETIMEDOUT;
     else if (o.status == RING_OK && (m.len >= (1ull << 32) || f > D.R)) o.status = RING_EMSGSIZE;
 
     bool locked = false;
     uint64_t P = L.tails[d];
-    const uint64_t t_start = globaltimer();
+    // %globaltimer is read only when a wait starts: a read costs ~0.7 us on
+    // B200 (measured with the put trace), far more than placing a message.
+    uint64_t t_start = (o.status == RING_OK && D.mpsc) ? globaltimer() : 0;
     if (o.status == RING_OK && D.mpsc) {
       // Step 1 "Acquire the lock using a CAS-based spinlock",
       // after our own previous items (and their Unlock) are published.
@@ -184,6 +190,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         // A PAD planned in this round must be published before waiting: the
         // consumer may have to free it for this message to fit (R3).
         st_release<false>(&S->planned, make_planned(L.items, L.units));
+        if (!t_start) t_start = globaltimer();
         uint64_t H3 = H2;
         while (H3 == H2) {
           if (globaltimer() - t_start > a.timeout_ns) break;
@@ -201,7 +208,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
     o.item = L.items++;
     o.flags = kStatus | (o.status == RING_OK ? kEntry : 0u) | (locked ? kUnlock : 0u);
     if (o.status == RING_OK) {
-      o.nunits = units_for(m.len, a.chunk);
+      o.nunits = m.nunits;
       o.first_unit = L.units;
       L.units += o.nunits;
     }
@@ -209,6 +216,86 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
     if (locked) return l + 1;
   }
   return gmax;
+}
+
+// Warp-parallel placement of one round for a single SPSC destination (no
+// router, no lock): the serial rule of leader_place evaluated for all lanes at
+// once.  Without a wrap, message l starts at P_b + (footprints of the messages
+// before it); at the first message that would cross R a PAD entry fills the
+// rest of the buffer region and the following messages start again from 0
+// (R3; an exact fit wraps to 0 without a PAD).  Every lane then
+// checks exactly the serial space rule (R4) and slot count (R5) at its own
+// position against the cached head; the leading run of lanes that fit is
+// placed.  Returns the run length; 0 leaves the round to the serial path
+// (credit wait, second wrap, EMSGSIZE).
+__device__ uint32_t fast_place(const PutArgs& a, LaunchCtx* ctx, LeaderState& L, uint32_t gmax, GroupSlot* gs,
+                               const MsgBrief* brief, const DestDesc& D) {
+  const int lane = threadIdx.x & 31;
+  const bool act = (uint32_t)lane < gmax;
+  const uint64_t f = act ? brief[lane].f : 0;
+  const uint64_t len = act ? brief[lane].len : 0;
+  if (__ballot_sync(0xffffffffu, act && (len >= (1ull << 32) || f > D.R))) return 0;
+  const uint64_t P = L.tails[0], H = L.heads[0];
+  const uint64_t pb = ptr_off(P), hb = ptr_off(H);
+  const uint32_t pq = ptr_seq(P), hq = ptr_seq(H);
+  const uint64_t incl = warp_incl_scan64(f, lane);
+  const uint64_t excl = incl - f;
+  const uint32_t wmask = __ballot_sync(0xffffffffu, act && pb + incl > D.R);
+  const uint32_t w = wmask ? (uint32_t)__ffs(wmask) - 1 : 32u;
+  const uint64_t excl_w = __shfl_sync(0xffffffffu, excl, w & 31);
+  const uint64_t pad_start = pb + excl_w;
+  const bool has_pad = w < 32 && pad_start < D.R;      // exact fit before w: no PAD
+  const uint32_t pad_seq = (pq + w) & kSeqMask;
+  uint64_t start;
+  uint32_t seq;
+  if ((uint32_t)lane < w) {
+    start = pb + excl;
+    seq = pq + lane;
+  } else {
+    start = excl - excl_w;
+    seq = pq + lane + (has_pad ? 1 : 0);
+  }
+  seq &= kSeqMask;
+  bool ok = act && start + f <= D.R && seq_dist(seq, hq) < D.N && span_free(start, seq, hb, hq, f);
+  if (has_pad && (uint32_t)lane >= w)
+    ok = ok && seq_dist(pad_seq, hq) < D.N && span_free(pad_start, pad_seq, hb, hq, D.R - pad_start);
+  const uint32_t notok = __ballot_sync(0xffffffffu, !ok);
+  const uint32_t run = notok ? (uint32_t)__ffs(notok) - 1 : 32u;
+  if (run == 0) return 0;
+  const bool pad_used = has_pad && w < run;
+  const bool c = (uint32_t)lane < run;
+  const uint32_t nu = c ? brief[lane].nunits : 0;
+  const uint32_t nu_incl = warp_incl_scan32(nu, lane);
+  const uint32_t items0 = L.items, units0 = L.units;
+  const uint64_t chan0 = L.chans[0];
+  const uint64_t tail_after = pack_ptr(advance(start, f, D.R), seq_inc(seq));
+  if (c) {
+    GroupSlot o = {};
+    o.start = start;
+    o.slot = seq;
+    o.tail_after = tail_after;
+    o.item = items0 + lane + ((pad_used && (uint32_t)lane >= w) ? 1 : 0);
+    o.dest = 0;
+    o.seq = (uint32_t)(chan0 + lane);
+    o.status = RING_OK;
+    o.flags = kStatus | kEntry;
+    o.nunits = nu;
+    o.first_unit = units0 + nu_incl - nu;
+    gs[lane] = o;
+  }
+  if (pad_used && (uint32_t)lane == w)
+    write_pad_plan(ctx, items0 + w, 0, pad_seq, kBusy | kPad | (D.R - pad_start), pack_ptr(0, seq_inc(pad_seq)));
+  const uint64_t last_tail = __shfl_sync(0xffffffffu, tail_after, run - 1);
+  const uint32_t nu_total = __shfl_sync(0xffffffffu, nu_incl, 31);
+  __syncwarp();
+  if (lane == 0) {
+    L.items = items0 + run + (pad_used ? 1 : 0);
+    L.units = units0 + nu_total;
+    L.chans[0] = chan0 + run;
+    L.tails[0] = last_tail;
+  }
+  __syncwarp();
+  return run;
 }
 
 __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const uint32_t* crc_tab) {
@@ -230,9 +317,12 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
     const uint32_t gmax = min((uint32_t)kGroup, a.n - k0);
     if ((uint32_t)lane < gmax) {   // stage the round's lengths / routing keys in parallel
       const ring_msg_t* mp = a.msgs ? a.msgs + k0 + lane : &a.inline_msg;
-      brief[lane].len = mp->len;
+      const uint64_t len = mp->len;
+      brief[lane].len = len;
+      brief[lane].f = footprint(len);
       brief[lane].app_id = mp->hdr.app_id;
       brief[lane].stage = mp->hdr.stage;
+      brief[lane].nunits = units_for(len, a.chunk);
     }
     __syncwarp();
     if (lane == 0) {
@@ -242,10 +332,27 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
         while (L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing)
           if (globaltimer() > end) { L.aborted = true; break; }
       }
-      s_g = leader_place(a, ctx, S, L, k0, gmax, gs, brief, s_dests);
+      const uint32_t rnd = k0 / kGroup;
+      if (a.trace && rnd < 64) a.trace[rnd * 4] = globaltimer();
+      // the fast path needs destination 0's state and a fresh credit
+      if (!a.routes && !s_dests[0].mpsc) {
+        if (!(L.loaded & 1u)) {
+          L.loaded |= 1u;
+          L.tails[0] = s_dests[0].st->tail_cache;
+          L.chans[0] = s_dests[0].st->chan_seq;
+        }
+        L.heads[0] = read_head(s_dests[0]);
+      }
     }
     __syncwarp();
-    const uint32_t g = s_g;
+    uint32_t g = 0;
+    if (!a.routes && !s_dests[0].mpsc && !L.aborted) g = fast_place(a, ctx, L, gmax, gs, brief, s_dests[0]);
+    if (g == 0) {
+      if (lane == 0) s_g = leader_place(a, ctx, S, L, k0, gmax, gs, brief, s_dests);
+      __syncwarp();
+      g = s_g;
+    }
+    if (lane == 0 && a.trace && k0 / kGroup < 64) a.trace[(k0 / kGroup) * 4 + 1] = globaltimer();
     if ((uint32_t)lane < g) {
       const uint32_t k = k0 + lane;
       const ring_msg_t m = a.msgs ? a.msgs[k] : a.inline_msg;
@@ -299,6 +406,8 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
       // One release hands the whole round (all lanes' plans, any PAD plans)
       // to the copy warps and the publisher.
       st_release<false>(&S->planned, make_planned(L.items, L.units));
+      const uint32_t rnd = k0 / kGroup;
+      if (a.trace && rnd < 64) { a.trace[rnd * 4 + 2] = globaltimer(); a.trace[rnd * 4 + 3] = g; }
     }
     k0 += g;
   }
@@ -315,8 +424,9 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
 // Steps 6-8 (WL, UH, Unlock), 32 items per look, in item order.
 __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   const int lane = threadIdx.x & 31;
-  uint32_t i = 0;
+  uint32_t i = 0, trace_n = 0;
   uint64_t idle_since = 0;
+  if (a.trace && lane == 0) a.trace[255] = globaltimer();
   while (true) {
     uint32_t ps = 0, done = 0;
     if (lane == 0) {
@@ -380,6 +490,11 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
       a.status[ld_cg32(&p.msg)] = ld_cg32(&p.status);
     }
     __syncwarp();
+    if (a.trace && lane == 0 && trace_n < 512) {
+      a.trace[256 + 2 * trace_n] = globaltimer();
+      a.trace[257 + 2 * trace_n] = ((uint64_t)i << 16) | run;
+      trace_n++;
+    }
     i += run;
     if (lane == 0) st_u32_release_gpu(&S->pub_seq, i);
   }

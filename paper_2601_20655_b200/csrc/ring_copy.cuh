@@ -29,7 +29,7 @@ __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8
     int4* d = reinterpret_cast<int4*>(dst);
     const uint32_t n16 = (uint32_t)(nb >> 4);
     uint32_t i = lane;
-    constexpr int U = 8;
+    constexpr int U = 16;   // 8 KiB in flight per warp
     for (; i + (U - 1) * 32 < n16; i += U * 32) {
       int4 v[U];
 #pragma unroll
@@ -61,15 +61,20 @@ __device__ __forceinline__ void reset_set(LaunchSet* s, int lane) {
   }
 }
 
-// Copy warp main loop.  Returns when the control warp is done and every unit
-// has been handed out, or after `2 * timeout_ns` without progress.
+// Copy warp main loop.  Units are dealt round robin: copy warp g of W takes
+// units g, g + W, g + 2W, ... (equal-sized units, so the static deal balances
+// and no warp contends on a shared counter).  Returns when the control warp is
+// done and no unit is left for this warp, or after `2 * timeout_ns` without
+// progress.  CTA 0 warps 0-1 are the control warps.
 __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns) {
   const int lane = threadIdx.x & 31;
-  uint32_t cur = 0;   // items before `cur` hold no unit this warp can still grab
-  while (true) {
-    uint32_t u = 0, quit = 0, ps = 0;
+  const uint32_t wpc = blockDim.x >> 5;
+  const uint32_t W = gridDim.x * wpc - 2;
+  const uint32_t g = blockIdx.x * wpc + (threadIdx.x >> 5) - 2;
+  uint32_t cur = 0;   // items before `cur` hold no unit this warp still needs
+  for (uint32_t unext = g;; unext += W) {
+    uint32_t u = unext, quit = 0, ps = 0;
     if (lane == 0) {
-      u = atomicAdd(&S->next_unit, 1u);
       uint64_t end = 0;
       // Poll with relaxed loads (no L1 invalidation per poll; thousands of
       // warps may wait here), then one acquire once the unit is planned.
@@ -126,8 +131,10 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t
   }
 }
 
+// `chunk` is a power of two (host-enforced): a shift, not a 64-bit division
+// (the division subroutine cost ~0.3 us per message in the serial leader path).
 __device__ __forceinline__ uint32_t units_for(uint64_t len, uint32_t chunk) {
-  const uint64_t u = (len + chunk - 1) / chunk;
+  const uint64_t u = (len + chunk - 1) >> (__ffs(chunk) - 1);
   return u ? (uint32_t)u : 1u;   // at least one: it also writes the header
 }
 

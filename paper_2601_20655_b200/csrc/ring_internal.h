@@ -107,7 +107,8 @@ struct PutArgs {
   LaunchCtx* ctx;
   const DestDesc* dests;
   Route* routes;
-  const uint32_t* crc_table;  // 256-entry CRC-32 byte table
+  const uint32_t* crc_table;  // CRC-32 slicing tables
+  uint64_t* trace;            // debug timeline (B200RING_TRACE=1), else null
   uint64_t timeout_ns;
   uint32_t launch;
   uint32_t n;

@@ -87,6 +87,7 @@ def _load():
         "ring_put_routed": [P, P, U32, U32, P, P, P],
         "ring_set_timeout_ns": [U64],
         "ring_clock_offset_ns": [I, C.POINTER(C.c_int64)],
+        "ring_peer_trace": [P, P, U32],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -190,6 +191,13 @@ def ring_peer_config(peer: int, copy_ctas: int = 0, threads: int = 0, copy_mode:
 
 def ring_peer_submitted(peer: int) -> int:
     return int(lib.ring_peer_submitted(peer))
+
+
+def ring_peer_trace(peer: int, n: int = 1280) -> np.ndarray:
+    """Debug timeline of the last put launch (needs B200RING_TRACE=1)."""
+    out = np.zeros(n, dtype=np.uint64)
+    _check("ring_peer_trace", lib.ring_peer_trace(peer, out.ctypes.data, n))
+    return out
 
 
 # ---- consumer ---------------------------------------------------------------------------
