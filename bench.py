@@ -171,19 +171,33 @@ def bench_c2(args):
         d_msgs.append(torch.from_numpy(a.view(np.uint8).copy()).cuda())
     status = torch.zeros(m, dtype=torch.int32, device="cuda")
     views = torch.zeros(m * 128, dtype=torch.uint8, device="cuda")
-    stream = torch.cuda.current_stream()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # Producer and consumer kernels on separate streams (configs[1]), streaming:
+    # consume(s) drains batch s while put(s) writes it, and put(s+1) (after
+    # put(s) on its stream) takes credit as consume(s) releases entries.  The
+    # waits form a chain, never a cycle: put(s+1) -> consume(s) -> put(s), and
+    # the consumer kernel is one warp, so it is always resident next to a put.
+    # With --no-overlap, put(s+1) waits for consume(s) to finish (event).
+    sp, sc = torch.cuda.Stream(), torch.cuda.Stream()
+    stream = sp
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    consumed = torch.cuda.Event()
+    consumed.record(sc)
 
-    def step(i, timed=None):
+    def step(i, timed=None, before_put=None):
+        if args.no_overlap or before_put is not None:
+            sp.wait_event(consumed)            # the previous batch has been consumed
+        if before_put is not None:
+            before_put()
         if timed is not None:
-            timed[0].record(stream)
-        R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, stream)
+            timed[0].record(sp)
+        R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
         if timed is not None:
-            timed[1].record(stream)
-        R.ring_consume(ring, m, views, None, 0, 0, stream)
+            timed[1].record(sp)
+            timed[2].record(sc)
+        R.ring_consume(ring, m, views, None, 0, 0, sc)
         if timed is not None:
-            timed[2].record(stream)
+            timed[3].record(sc)
+        consumed.record(sc)
 
     for i in range(args.warmup):
         step(i)
@@ -196,16 +210,18 @@ def bench_c2(args):
     l0 = R.ring_launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    t_start.record(stream)
+    t_start.record(sp)
+    sc.wait_event(t_start)
     for i in range(args.steps):
         step(args.warmup + i, ev[i])
-    t_end.record(stream)
+    sp.wait_stream(sc)
+    t_end.record(sp)
     torch.cuda.synchronize()
     launches = R.ring_launch_count() - l0
     clocks = clk.stop()
     ms = t_start.elapsed_time(t_end)
-    put_ms = [a.elapsed_time(b) for a, b, c in ev]
-    get_ms = [b.elapsed_time(c) for a, b, c in ev]
+    put_ms = [a.elapsed_time(b) for a, b, c, d in ev]
+    get_ms = [c.elapsed_time(d) for a, b, c, d in ev]
     assert (status == 0).all().item()
     v = R.parse_views(views.cpu().numpy())
     assert (v["status"] == 0).all()
@@ -226,10 +242,14 @@ def bench_c2(args):
     host_views = torch.empty(m * 128, dtype=torch.uint8).pin_memory()
     e_steps = max(3, min(args.steps, 50))
 
+    def h2d():
+        with torch.cuda.stream(sp):
+            src[: m * stride].copy_(host_src, non_blocking=True)
+
     def e2e_step():
-        src[: m * stride].copy_(host_src, non_blocking=True)
-        step(0)
-        host_views.copy_(views, non_blocking=True)
+        step(0, before_put=h2d)              # source set 0 = the buffer just copied in
+        with torch.cuda.stream(sc):
+            host_views.copy_(views, non_blocking=True)
 
     for i in range(2):
         e2e_step()
@@ -238,6 +258,7 @@ def bench_c2(args):
     e0.record(stream)
     for i in range(e_steps):
         e2e_step()
+    sp.wait_stream(sc)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e = m * plen * e_steps / (e0.elapsed_time(e1) / 1e3) / 1e9
@@ -253,7 +274,9 @@ def bench_c2(args):
                                "(R=64 MiB), 1,048,512-B payloads (footprint 1 MiB), put batch -> consume batch",
                    "R_bytes": Rb, "n_slots": N, "msgs_per_step": m, "payload_bytes": plen,
                    "l2": "inputs larger than L2 (4 x 64 MiB rotating source sets + 64 MiB ring)",
-                   "consume_mode": "view (zero copy)", "parallelism": "replicas only (1 ring)"},
+                   "consume_mode": "view (zero copy)", "parallelism": "replicas only (1 ring)",
+                   "streams": "put on one stream, consume on another; consume(s) overlaps put(s), "
+                              "put(s+1) waits for consume(s) (event)"},
         "msgs_per_s": round(m * args.steps / (ms / 1e3), 1),
         "latency_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99),
                        "what": "t_visible - t_put of the last step's 64 messages (same GPU clock; batched put, "
@@ -486,6 +509,7 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--lat-iters", type=int, default=40)
+    ap.add_argument("--no-overlap", action="store_true", help="N=1: put(s+1) waits for consume(s)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

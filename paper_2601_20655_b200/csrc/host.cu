@@ -461,7 +461,14 @@ static void default_grid(int device, bool sys, uint32_t* ctas, uint32_t* threads
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
   if (!*ctas) *ctas = sys ? 33u : (uint32_t)nsm;
   if (!*threads) *threads = 512;
-  if (!*chunk) *chunk = 32u << 10;
+  if (!*chunk) {
+    *chunk = 32u << 10;
+    // tuning knob (power of two, 4 KiB .. 1 MiB)
+    if (const char* e = getenv("B200RING_CHUNK")) {
+      const unsigned long v = strtoul(e, nullptr, 0);
+      if (v >= 4096 && v <= (1u << 20) && !(v & (v - 1))) *chunk = (uint32_t)v;
+    }
+  }
 }
 
 static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const ring_msg_t* inline_msg, uint32_t n,

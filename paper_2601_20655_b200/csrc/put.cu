@@ -116,8 +116,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
 
     bool locked = false;
     uint64_t P = L.tails[d];
-    // %globaltimer is read only when a wait starts: a read costs ~0.7 us on
-    // B200 (measured with the put trace), far more than placing a message.
+    // %globaltimer is read only when a wait starts (keeps the serial path lean).
     uint64_t t_start = (o.status == RING_OK && D.mpsc) ? globaltimer() : 0;
     if (o.status == RING_OK && D.mpsc) {
       // Step 1 "Acquire the lock using a CAS-based spinlock",
@@ -421,32 +420,58 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
   }
 }
 
-// Steps 6-8 (WL, UH, Unlock), 32 items per look, in item order.
+// Steps 6-8 (WL, UH, Unlock), 32 items per look, in item order.  Lane l
+// caches the plan of item i + l (read once); each look only polls the arrive
+// counters.  For the leading run of complete items: the lanes write the size
+// slots (WL), ONE fence orders the payload copies (observed through the
+// arrive counters) and the slots before the tail store (UH) and pub_seq.
 __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   const int lane = threadIdx.x & 31;
-  uint32_t i = 0, trace_n = 0;
+  uint32_t i = 0, trace_n = 0, ps = 0, done = 0;
   uint64_t idle_since = 0;
+  bool have = false;
+  uint32_t flags = 0, dest = 0, nunits = 0, slot = 0, msg = 0, status = 0;
+  uint64_t slot_word = 0, tail_after = 0;
   if (a.trace && lane == 0) a.trace[255] = globaltimer();
   while (true) {
-    uint32_t ps = 0, done = 0;
-    if (lane == 0) {
-      done = ld_acquire_gpu32(&S->done);   // before `planned`: final once done is seen
-      ps = planned_items(ld_acquire<false>(&S->planned));
-    }
-    __syncwarp();
-    ps = __shfl_sync(0xffffffffu, ps, 0);
-    done = __shfl_sync(0xffffffffu, done, 0);
-    if (i >= ps && done) break;
     const uint32_t j = i + lane;
-    bool ready = false;
-    uint32_t flags = 0, dest = 0, nunits = 0;
-    if (j < ps) {
+    // Independent loads in one pass: lane 0 looks for newly planned items (relaxed),
+    // every lane with a cached item polls its arrive counter (relaxed).
+    uint64_t pl = 0;
+    uint32_t dn = 0, arr = 0;
+    if (lane == 0 && !done) {
+      dn = ld_relaxed_gpu32(&S->done);
+      pl = ld_relaxed<false>(&S->planned);
+    }
+    if (have && nunits) arr = ld_relaxed_gpu32(&S->arrive[j % kPlanRing]);
+    dn = __shfl_sync(0xffffffffu, dn, 0);
+    pl = __shfl_sync(0xffffffffu, pl, 0);
+    if (!done && (dn || planned_items(pl) != ps)) {
+      // acquire the newer plans (done is released after the final `planned`)
+      uint32_t p = 0;
+      if (lane == 0) {
+        if (dn) (void)ld_acquire_gpu32(&S->done);
+        p = planned_items(ld_acquire<false>(&S->planned));
+      }
+      __syncwarp();
+      ps = __shfl_sync(0xffffffffu, p, 0);
+      done = dn;
+    }
+    if (i >= ps && done) break;
+    if (!have && j < ps) {
       const Plan& p = ctx->plan[j % kPlanRing];
       flags = ld_cg32(&p.flags);
       dest = ld_cg32(&p.dest);
       nunits = ld_cg32(&p.nunits);
-      ready = nunits == 0 || ld_acquire_gpu32(&S->arrive[j % kPlanRing]) == nunits;
+      slot = ld_cg32(&p.slot);
+      msg = ld_cg32(&p.msg);
+      status = ld_cg32(&p.status);
+      slot_word = ld_cg64(&p.slot_word);
+      tail_after = ld_cg64(&p.tail_after);
+      have = true;
+      if (nunits) arr = ld_relaxed_gpu32(&S->arrive[j % kPlanRing]);
     }
+    const bool ready = have && (nunits == 0 || arr == nunits);
     const uint32_t notready = __ballot_sync(0xffffffffu, !ready);
     uint32_t run = notready ? __ffs(notready) - 1 : 32;
     // a run stays on one destination and ends at an Unlock
@@ -463,40 +488,44 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     }
     idle_since = 0;
     const DestDesc& D = a.dests[dest0];
-    if ((uint32_t)lane < run) {
-      const Plan& p = ctx->plan[j % kPlanRing];
-      if (nunits) S->arrive[j % kPlanRing] = 0;
-      if (flags & kEntry) {   // WL: size + busy bit (PAD entries carry the pad bit)
-        const uint64_t word = ld_cg64(&p.slot_word);
-        const uint32_t slot = ld_cg32(&p.slot);
-        if (D.sys) st_relaxed<true>(slot_w(D, slot), word);
-        else st_relaxed<false>(slot_w(D, slot), word);
-      }
+    const bool mine = (uint32_t)lane < run;
+    if (mine && nunits) S->arrive[j % kPlanRing] = 0;
+    if (mine && (flags & kEntry)) {   // WL: size + busy bit (PAD entries carry the pad bit)
+      if (D.sys) st_relaxed<true>(slot_w(D, slot), slot_word);
+      else st_relaxed<false>(slot_w(D, slot), slot_word);
     }
-    const uint32_t entries = __ballot_sync(0xffffffffu, (uint32_t)lane < run && (flags & kEntry));
-    __syncwarp();
+    const uint32_t entries = __ballot_sync(0xffffffffu, mine && (flags & kEntry));
+    const uint64_t tail = __shfl_sync(0xffffffffu, tail_after, entries ? 31 - __clz(entries) : 0);
+    // acquire for the arrive counters read above, release for the copies and slots
+    if (D.sys) fence_acq_rel<true>(); else fence_acq_rel<false>();
     if (lane == 0) {
-      if (entries) {   // UH: one release covers the run's entries
-        const uint32_t last = 31 - __clz(entries);
-        const uint64_t tail = ld_cg64(&ctx->plan[(i + last) % kPlanRing].tail_after);
-        if (D.sys) st_release<true>(tail_w(D), tail); else st_release<false>(tail_w(D), tail);
+      if (entries) {   // UH: one fence covers the run's entries
+        if (D.sys) st_relaxed<true>(tail_w(D), tail); else st_relaxed<false>(tail_w(D), tail);
       }
       if (unl && (uint32_t)__ffs(unl) == run) {   // Unlock after the tail
         if (D.sys) st_release<true>(lock_w(D), 0ull); else st_release<false>(lock_w(D), 0ull);
       }
     }
-    if ((uint32_t)lane < run && (flags & kStatus)) {
-      const Plan& p = ctx->plan[j % kPlanRing];
-      a.status[ld_cg32(&p.msg)] = ld_cg32(&p.status);
-    }
-    __syncwarp();
+    if (mine && (flags & kStatus)) a.status[msg] = status;
     if (a.trace && lane == 0 && trace_n < 512) {
       a.trace[256 + 2 * trace_n] = globaltimer();
       a.trace[257 + 2 * trace_n] = ((uint64_t)i << 16) | run;
       trace_n++;
     }
     i += run;
-    if (lane == 0) st_u32_release_gpu(&S->pub_seq, i);
+    if (lane == 0) st_u32_relaxed_gpu(&S->pub_seq, i);
+    // slide the window by `run`
+    const uint32_t src = min((uint32_t)lane + run, 31u);
+    const bool h2 = __shfl_sync(0xffffffffu, have, src) && (uint32_t)lane + run < 32;
+    flags = __shfl_sync(0xffffffffu, flags, src);
+    dest = __shfl_sync(0xffffffffu, dest, src);
+    nunits = __shfl_sync(0xffffffffu, nunits, src);
+    slot = __shfl_sync(0xffffffffu, slot, src);
+    msg = __shfl_sync(0xffffffffu, msg, src);
+    status = __shfl_sync(0xffffffffu, status, src);
+    slot_word = __shfl_sync(0xffffffffu, slot_word, src);
+    tail_after = __shfl_sync(0xffffffffu, tail_after, src);
+    have = h2;
   }
 }
 

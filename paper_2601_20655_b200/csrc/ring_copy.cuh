@@ -61,20 +61,19 @@ __device__ __forceinline__ void reset_set(LaunchSet* s, int lane) {
   }
 }
 
-// Copy warp main loop.  Units are dealt round robin: copy warp g of W takes
-// units g, g + W, g + 2W, ... (equal-sized units, so the static deal balances
-// and no warp contends on a shared counter).  Returns when the control warp is
-// done and no unit is left for this warp, or after `2 * timeout_ns` without
-// progress.  CTA 0 warps 0-1 are the control warps.
+// Copy warp main loop: take the next unit with one atomicAdd (dynamic,
+// warp-granular scheduling).  Only warps that are resident take units, so the
+// launch makes progress even if some of its CTAs cannot be scheduled (other
+// kernels occupying SMs): the kernel never needs all its CTAs co-resident.
+// Returns when the control warp is done and every unit has been handed out, or
+// after `2 * timeout_ns` without progress.
 __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns) {
   const int lane = threadIdx.x & 31;
-  const uint32_t wpc = blockDim.x >> 5;
-  const uint32_t W = gridDim.x * wpc - 2;
-  const uint32_t g = blockIdx.x * wpc + (threadIdx.x >> 5) - 2;
-  uint32_t cur = 0;   // items before `cur` hold no unit this warp still needs
-  for (uint32_t unext = g;; unext += W) {
-    uint32_t u = unext, quit = 0, ps = 0;
+  uint32_t cur = 0;   // items before `cur` hold no unit this warp can still take
+  while (true) {
+    uint32_t u = 0, quit = 0, ps = 0;
     if (lane == 0) {
+      u = atomicAdd(&S->next_unit, 1u);
       uint64_t end = 0;
       // Poll with relaxed loads (no L1 invalidation per poll; thousands of
       // warps may wait here), then one acquire once the unit is planned.
