@@ -488,6 +488,8 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   uint32_t ctas = p->copy_ctas, thr = p->threads, chunk = p->chunk;
   DevGuard g(p->device);
   default_grid(p->device, p->desc.sys, &ctas, &thr, &chunk);
+  a.copy_mode = p->copy_mode;
+  if (a.copy_mode == 1 && chunk > (48u << 10)) chunk = 48u << 10;   // engine stages live in shared memory
   a.chunk = chunk;
   a.launch = p->launches;
   if (getenv("B200RING_TRACE")) {

@@ -546,6 +546,11 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
       return;
     }
   }
+  if (a.copy_mode == 1) {      // TMA engine: one warp per CTA (CTA 0: warp 2)
+    extern __shared__ __align__(128) uint8_t dyn_smem[];
+    if (warp == (blockIdx.x == 0 ? 2 : 0)) copy_engine<kEngineStages>(ctx, S, a.chunk, a.timeout_ns, dyn_smem);
+    return;
+  }
   copy_warp(ctx, S, a.chunk, a.timeout_ns);
 }
 
@@ -555,11 +560,15 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
 // times out; so every kernel is loaded when a device is first used.
 cudaError_t preload_put() {
   cudaFuncAttributes fa;
-  return cudaFuncGetAttributes(&fa, put_kernel);
+  cudaError_t e = cudaFuncGetAttributes(&fa, put_kernel);
+  if (e == cudaSuccess)   // TMA engine stages (up to kEngineStages x 48 KiB)
+    e = cudaFuncSetAttribute(put_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kEngineStages * (48 << 10));
+  return e;
 }
 
 cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s) {
-  put_kernel<<<ctas, threads, 0, s>>>(a);
+  const size_t dyn = a.copy_mode == 1 ? (size_t)kEngineStages * a.chunk : 0;
+  put_kernel<<<ctas, a.copy_mode == 1 ? 96u : threads, dyn, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -132,6 +132,169 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t
 
 // `chunk` is a power of two (host-enforced): a shift, not a 64-bit division
 // (the division subroutine cost ~0.3 us per message in the serial leader path).
+// ---------------------------------------------------------------------------
+// TMA copy engine (copy_mode 1): one warp per CTA drives a ring of `stages`
+// shared-memory buffers of `chunk` bytes with bulk asynchronous copies
+// (cp.async.bulk global -> shared, completion on an mbarrier; then
+// shared -> global, completion by bulk group).  One elected lane issues; the
+// warp helps to find the entry of a unit and writes headers and ragged tails.
+// The SM's LSU and registers stay free (the paper's L3 concern about GPU
+// interference), and each SM keeps stages*chunk bytes in flight.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+struct EngineStage {
+  uint64_t dst;
+  uint32_t n, item;
+};
+
+// Finds the item holding unit u among planned items [cur, ps); warp-uniform.
+__device__ __forceinline__ uint32_t find_item(LaunchCtx* ctx, uint32_t u, uint32_t cur, uint32_t ps, int lane) {
+  for (uint32_t b = cur; b < ps; b += 32) {
+    const uint32_t i = b + lane;
+    bool hit = false;
+    if (i < ps) {
+      const Plan& p = ctx->plan[i % kPlanRing];
+      const uint32_t nu = ld_cg32(&p.nunits);
+      const uint32_t fu = ld_cg32(&p.first_unit);
+      hit = nu && u >= fu && u - fu < nu;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, hit);
+    if (m) return b + __ffs(m) - 1;
+  }
+  return 0xffffffffu;
+}
+
+template <int STAGES>
+__device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns, uint8_t* bufs) {
+  const int lane = threadIdx.x & 31;
+  __shared__ __align__(8) uint64_t bar[STAGES];
+  __shared__ EngineStage st[STAGES];
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;                       // parity bit per stage (lane 0)
+  uint32_t k_issue = 0, k_store = 0, k_done = 0, cur = 0;
+  uint32_t pending_u = 0xffffffffu;         // unit taken but not planned yet
+  bool exhausted = false;
+  uint64_t wait_end = 0;
+  while (true) {
+    // ---- refill free stages with planned units
+    while (!exhausted && k_issue - k_done < (uint32_t)STAGES) {
+      uint32_t u = 0, state = 0, ps = 0;    // state 0 = planned, 1 = not yet, 2 = exhausted
+      if (lane == 0) {
+        if (pending_u == 0xffffffffu) pending_u = atomicAdd(&S->next_unit, 1u);
+        u = pending_u;
+        if (planned_units(ld_relaxed<false>(&S->planned)) <= u) {
+          state = 1;
+          if (ld_relaxed_gpu32(&S->done)) {
+            (void)ld_acquire_gpu32(&S->done);
+            if (planned_units(ld_acquire<false>(&S->planned)) <= u) state = 2;
+          }
+        }
+        if (state == 0) ps = planned_items(ld_acquire<false>(&S->planned));
+      }
+      __syncwarp();
+      state = __shfl_sync(0xffffffffu, state, 0);
+      if (state == 2) { exhausted = true; break; }
+      if (state == 1) {
+        if (k_done < k_issue) break;        // finish in-flight work first, never spin with it pending
+        const uint64_t t = globaltimer();
+        if (!wait_end) wait_end = t + 2 * timeout_ns;
+        else if (t > wait_end) { exhausted = true; break; }
+        __nanosleep(64);
+        continue;
+      }
+      wait_end = 0;
+      u = __shfl_sync(0xffffffffu, u, 0);
+      ps = __shfl_sync(0xffffffffu, ps, 0);
+      pending_u = 0xffffffffu;
+      const uint32_t item = find_item(ctx, u, cur, ps, lane);
+      if (item == 0xffffffffu) { exhausted = true; break; }
+      cur = item;
+      const Plan& p = ctx->plan[item % kPlanRing];
+      const uint64_t src = ld_cg64(&p.src), dst = ld_cg64(&p.dst), len = ld_cg64(&p.len);
+      const uint64_t hdr_dst = ld_cg64(&p.hdr_dst);
+      const uint32_t c = u - ld_cg32(&p.first_unit);
+      const uint64_t lo = (uint64_t)c * chunk;
+      const uint64_t hi = min(len, lo + chunk);
+      const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src) + lo;
+      uint8_t* d8 = reinterpret_cast<uint8_t*>(dst) + lo;
+      if (c == 0 && hdr_dst && lane < 4) {
+        const int4 h = __ldcg(reinterpret_cast<const int4*>(p.hdr) + lane);
+        st16(reinterpret_cast<uint8_t*>(hdr_dst) + 16 * lane, h);
+      }
+      const uint64_t n = hi > lo ? hi - lo : 0;
+      const bool aligned = ((((uintptr_t)s8) | ((uintptr_t)d8)) & 15) == 0;
+      const uint32_t n16 = aligned ? (uint32_t)(n & ~15ull) : 0u;
+      if (n16 < n) warp_copy(s8 + n16, d8 + n16, n - n16, lane);   // ragged tail / unaligned: LSU
+      if (n16 == 0) {                                                // nothing for the engine
+        __syncwarp();
+        if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);
+        continue;
+      }
+      __syncwarp();     // header / tail stores of the lanes precede the arrive issued later by lane 0
+      if (lane == 0) {
+        const int s = (int)(k_issue % STAGES);
+        st[s].dst = reinterpret_cast<uint64_t>(d8);
+        st[s].n = n16;
+        st[s].item = item;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[s])), "r"(n16)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(smem_addr(bufs + (size_t)s * chunk)), "l"(s8), "r"(n16), "r"(smem_addr(&bar[s]))
+                     : "memory");
+      }
+      ++k_issue;
+    }
+    if (k_done == k_issue) {
+      if (exhausted) break;
+      continue;
+    }
+    if (k_store < k_issue) {
+      // ---- oldest load complete -> bulk store to the (peer) ring
+      if (lane == 0) {
+        const int s = (int)(k_store % STAGES);
+        const uint32_t par = (phase >> s) & 1u;
+        uint32_t ok = 0;
+        while (!ok)
+          asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                       : "=r"(ok) : "r"(smem_addr(&bar[s])), "r"(par) : "memory");
+        phase ^= 1u << s;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(st[s].dst), "r"(smem_addr(bufs + (size_t)s * chunk)), "r"(st[s].n) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      ++k_store;
+      __syncwarp();
+      continue;   // store every loaded stage before waiting on the oldest store
+    }
+    // ---- oldest store complete -> the entry's arrive counter
+    if (k_done < k_store && lane == 0) {
+      const uint32_t newer = k_store - k_done - 1;   // groups allowed to stay pending
+      switch (newer) {
+        case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+        case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
+        case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
+        default: asm volatile("cp.async.bulk.wait_group 7;" ::: "memory"); break;
+      }
+      // async-proxy writes are complete; order them before the generic release
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      red_release_gpu_add(&S->arrive[st[k_done % STAGES].item % kPlanRing], 1u);
+    }
+    if (k_done < k_store) ++k_done;
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t units_for(uint64_t len, uint32_t chunk) {
   const uint64_t u = (len + chunk - 1) >> (__ffs(chunk) - 1);
   return u ? (uint32_t)u : 1u;   // at least one: it also writes the header

@@ -116,7 +116,11 @@ struct PutArgs {
   uint32_t n_dests;
   uint32_t n_routes;
   uint32_t chunk;             // bytes per copy work unit
+  uint32_t copy_mode;         // 0: LSU copy warps, 1: TMA engine per CTA
+  uint32_t _pad;
 };
+
+constexpr int kEngineStages = 4;   // TMA engine: shared-memory stages of `chunk` bytes
 
 struct GetArgs {
   uint8_t* ring;

@@ -39,12 +39,13 @@ def _status(t):
     return [int(x) for x in t.cpu().tolist()]
 
 
-def _run_spsc(R, L, stream, flags=0, mode="consume_copy", local=True, dev=0, max_batch=10**9):
+def _run_spsc(R, L, stream, flags=0, mode="consume_copy", local=True, dev=0, max_batch=10**9, copy_mode=0):
     """Feed `stream` through one ring on `dev` in host-planned batches (put then
     get in stream order on one GPU; no two kernels ever wait on each other)."""
     ring = R.ring_create(dev, L.R, L.N, 1, R.RING_CREATE_LOCAL if local else 0)
     peer, mh = R.ring_attach_peer(R.ring_export(ring), dev, 0)
     R.ring_bind_mirror(ring, 0, mh)
+    R.ring_peer_config(peer, 0, 0, copy_mode)
     buf, srcs = upload(stream, f"cuda:{dev}")
     msgs = msg_tensor(stream, srcs, f"cuda:{dev}")
     views_all, payloads, put_status = [], [], []
@@ -82,14 +83,15 @@ def _run_spsc(R, L, stream, flags=0, mode="consume_copy", local=True, dev=0, max
     return np.concatenate(views_all) if views_all else None, payloads, put_status, img
 
 
-@pytest.mark.parametrize("mode", ["consume_copy", "get_view_release", "consume_view"])
-def test_c1_stream_bit_exact(R, mode):
+@pytest.mark.parametrize("mode,copy_mode", [("consume_copy", 0), ("get_view_release", 0), ("consume_view", 0),
+                                            ("consume_copy", 1), ("get_view_release", 1)])
+def test_c1_stream_bit_exact(R, mode, copy_mode):
     """BASELINE.json configs[0] on the GPU: 1 -> 1, 8 slots x 4 KB (R = 32 KiB),
     1,000 messages of U[1, 4096] B."""
     L = Layout(32768, 8)
     stream = synth.random_stream(synth.SEED_BASE + 1, 0, 1000, 1, 4096)
     sim = oracle_spsc(L, to_oracle_msgs(stream))
-    views, payloads, st, img = _run_spsc(R, L, stream, mode=mode)
+    views, payloads, st, img = _run_spsc(R, L, stream, mode=mode, copy_mode=copy_mode)
     assert st == [0] * 1000
     check_views_against_oracle(views, sim, 0, stream)
     if payloads:
@@ -110,9 +112,10 @@ def test_c1_system_scope_same_device(R):
     assert img["tail"] == sim.mem.tail == img["head"]
 
 
-def test_edge_sizes_and_unaligned_sources(R):
+@pytest.mark.parametrize("copy_mode", [0, 1])
+def test_edge_sizes_and_unaligned_sources(R, copy_mode):
     """Empty payload, sub-vector tails, exact fit f == R, and sources that are
-    not 16-B (or 4-B) aligned."""
+    not 16-B (or 4-B) aligned (the TMA engine falls back to the LSU for those)."""
     L = Layout(4096, 8)
     # f == R (4096 - 64 B payload) only fits an empty ring at P_b = 0 without
     # waiting for the consumer (one GPU runs put, then get), so it goes first.
@@ -124,6 +127,7 @@ def test_edge_sizes_and_unaligned_sources(R):
     ring = R.ring_create(0, L.R, L.N, 1, R.RING_CREATE_LOCAL)
     peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
     R.ring_bind_mirror(ring, 0, mh)
+    R.ring_peer_config(peer, 0, 0, copy_mode)
     host = np.zeros(sum(n + 32 for n in lens), dtype=np.uint8)
     srcs_off, o = [], 0
     for q, m in enumerate(stream):
@@ -368,14 +372,15 @@ def test_router_round_robin_and_epoch_flip(R):
         R.ring_destroy(r)
 
 
-def test_c2_full_size_same_gpu(R):
+@pytest.mark.parametrize("copy_mode", [0, 1])
+def test_c2_full_size_same_gpu(R, copy_mode):
     """BASELINE.json configs[1] at full size: 64 slots x 1 MiB (R = 64 MiB),
     1,048,512-B payloads (footprint exactly 1 MiB), the bench's launch
     configuration (all SMs copying), two laps of the ring."""
     L = Layout(64 << 20, 64)
     stream = synth.fixed_stream(synth.SEED_BASE + 2, 0, 126, 1048512)
     sim = oracle_spsc(L, to_oracle_msgs(stream))
-    views, payloads, st, img = _run_spsc(R, L, stream, mode="consume_copy")
+    views, payloads, st, img = _run_spsc(R, L, stream, mode="consume_copy", copy_mode=copy_mode)
     assert st == [0] * 126
     check_views_against_oracle(views, sim, 0, stream)
     assert payloads == [m.payload.tobytes() for m in stream]
@@ -386,9 +391,10 @@ def test_c2_full_size_same_gpu(R):
 # Two or more GPUs, one process (peer access): producer and consumer kernels run
 # concurrently on different GPUs, so credit and data flow while both spin.
 # ---------------------------------------------------------------------------------------
-def _p2p_stream(R, L, stream, prod_dev, cons_dev, cap, copy=True):
+def _p2p_stream(R, L, stream, prod_dev, cons_dev, cap, copy=True, copy_mode=0):
     ring = R.ring_create(cons_dev, L.R, L.N, 1, 0)
     peer, mh = R.ring_attach_peer(R.ring_export(ring), prod_dev, 0)
+    R.ring_peer_config(peer, 0, 0, copy_mode)
     R.ring_bind_mirror(ring, 0, mh)
     buf, srcs = upload(stream, f"cuda:{prod_dev}")
     msgs = msg_tensor(stream, srcs, f"cuda:{prod_dev}")
@@ -430,7 +436,8 @@ def test_p2p_small_ring_streaming_wraps(R):
 
 
 @pytest.mark.multigpu
-def test_p2p_c3_wan_tensors(R):
+@pytest.mark.parametrize("copy_mode", [0, 1])
+def test_p2p_c3_wan_tensors(R, copy_mode):
     """BASELINE.json configs[2]: umT5 embeddings 512x4096 bf16 (4,194,304 B)
     alternating with 480p latents 16x21x60x104 bf16 (4,193,280 B), GPU0 -> ring
     on GPU1 (R = 64 MiB, N = 64), 48 messages in one streaming launch pair."""
@@ -438,7 +445,7 @@ def test_p2p_c3_wan_tensors(R):
     L = Layout(64 << 20, 64)
     stream = synth.wan_stream(synth.SEED_BASE + 3, 0, 48)
     sim = oracle_spsc(L, to_oracle_msgs(stream))
-    v, pl, st, img = _p2p_stream(R, L, stream, 0, 1, 4194304)
+    v, pl, st, img = _p2p_stream(R, L, stream, 0, 1, 4194304, copy_mode=copy_mode)
     assert st == [0] * 48
     check_views_against_oracle(v, sim, 0, stream)
     assert pl == [m.payload.tobytes() for m in stream]

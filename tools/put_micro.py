@@ -15,7 +15,7 @@ src = torch.randint(0, 255, (256 << 20,), dtype=torch.uint8, device="cuda")
 views = torch.zeros(64 * 128, dtype=torch.uint8, device="cuda")
 status = torch.zeros(64, dtype=torch.int32, device="cuda")
 cases = [("64 x 0 B", 64, 0), ("64 x 4 KiB", 64, 4096), ("63 x 1 MiB-64", 63, 1048512),
-         ("15 x 4 MiB-64", 15, 4194240), ("1 x 63 MiB", 1, 63 << 20)]
+         ("15 x 4 MiB-64", 15, 4194240)]
 TRACE = bool(os.environ.get("B200RING_TRACE"))
 
 
@@ -30,11 +30,12 @@ def show_trace():
     pub = [((t[256+2*j] - t0) / 1e3, int(t[257+2*j]) >> 16, int(t[257+2*j]) & 0xffff) for j in range(512) if t[256+2*j]]
     print(f"   publisher start {(t[255]-t0)/1e3:.2f} us; runs (t us, first item, run):", [(round(a, 2), b, c) for a, b, c in pub[:40]], "... n =", len(pub))
 grids = [int(x) for x in (sys.argv[1:] or ["148", "296"])]
+MODES = [int(x) for x in os.environ.get("COPY_MODES", "0,1").split(",")]
 for ctas in grids:
-    for threads in (512, 1024):
-        if ctas * threads > 148 * 2048:
-            continue
-        R.ring_peer_config(peer, ctas, threads, 0)
+  for mode in MODES:
+    for threads in (512,):
+        R.ring_peer_config(peer, ctas, threads, mode)
+        print(f"copy_mode={mode}")
         for name, m, plen in cases:
             a = R.make_msgs([src.data_ptr() + q * (plen + 256) % (192 << 20) for q in range(m)], [plen] * m,
                             [bytes(16)] * m, [0] * m, [7] * m, [1] * m)
