@@ -157,8 +157,8 @@ def bench_c2(args):
     ring = R.ring_create(dev, Rb, N, 1, R.RING_CREATE_LOCAL)
     peer, mh = R.ring_attach_peer(R.ring_export(ring), dev, 0)
     R.ring_bind_mirror(ring, 0, mh)
-    if args.ctas or args.threads:
-        R.ring_peer_config(peer, args.ctas, args.threads, 0)
+    if args.ctas or args.threads or args.copy_mode:
+        R.ring_peer_config(peer, args.ctas, args.threads, args.copy_mode)
     stride = (plen + 255) // 256 * 256
     src = torch.empty(sets * m * stride, dtype=torch.uint8, device="cuda")
     for k in range(sets * m):
@@ -303,19 +303,18 @@ def bench_pairs(args, rank, world, grp):
     import synth
     from paper_2601_20655_b200 import ring as R
 
+    from paper_2601_20655_b200 import topology as T
     dev = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(dev)
     Rb, N = 64 << 20, 64
     m = args.msgs_per_step or 32
-    ring = R.ring_create(dev, Rb, N, 1, 0)
-    handles = [None] * world
-    dist.all_gather_object(handles, R.ring_export(ring), group=grp)
-    peer, mh = R.ring_attach_peer(handles[(rank + 1) % world], dev, 0)
-    if args.ctas or args.threads:
-        R.ring_peer_config(peer, args.ctas, args.threads, 0)
-    mirrors = [None] * world
-    dist.all_gather_object(mirrors, mh, group=grp)
-    R.ring_bind_mirror(ring, 0, mirrors[(rank - 1) % world])
+    wired = T.wire(T.plan_pairs(world, Rb, N), rank, world, grp, device=dev,
+                   create=lambda s, d: R.ring_create(d, s.data_bytes, s.n_slots, s.max_producers, 0),
+                   export=R.ring_export, attach=R.ring_attach_peer, bind=R.ring_bind_mirror)
+    ring = wired.rings[f"in{rank}"]
+    peer = wired.peers[f"in{(rank + 1) % world}"]
+    if args.ctas or args.threads or args.copy_mode:
+        R.ring_peer_config(peer, args.ctas, args.threads, args.copy_mode)
     offsets = [None] * world
     dist.all_gather_object(offsets, R.ring_clock_offset_ns(dev), group=grp)
     log("rings attached; clock offsets (gpu - host, ns):", offsets)
@@ -507,6 +506,10 @@ def main():
     ap.add_argument("--msgs-per-step", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0, help="put grid size (0 = library default)")
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--copy-mode", type=int, default=0, help="0: LSU copy warps, 1: TMA engine")
+    ap.add_argument("--topology", default="pairs", choices=["pairs", "pipeline", "fanin", "reassign"],
+                    help="N>1: pairs (default bench line) or the C4 / C5a / C5b runs of bench_multi.py")
+    ap.add_argument("--sizes", default="", help="fanin: comma-separated message sizes")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--lat-iters", type=int, default=40)
     ap.add_argument("--no-overlap", action="store_true", help="N=1: put(s+1) waits for consume(s)")
@@ -534,7 +537,13 @@ def main():
     dist.init_process_group("nccl")
     grp = dist.new_group(backend="gloo")
     try:
-        out = bench_pairs(args, rank, world, grp)
+        if args.topology != "pairs":
+            import bench_multi
+            if not args.steps or args.steps == 200:
+                args.steps = 10
+            out = bench_multi.main(args, rank, world, grp)
+        else:
+            out = bench_pairs(args, rank, world, grp)
         if out:
             print(json.dumps(out), flush=True)
     finally:
