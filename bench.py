@@ -56,6 +56,20 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def ncu_traffic(name: str, kernel: str = "put_kernel"):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from
+    the committed summary of one `ncu --set full` capture of the same bench
+    command (profiles/<name>, written by tools/ncu_summary.py), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            for d in json.load(f):
+                if kernel in d.get("kernel", "") and "dram_traffic_bytes" in d:
+                    return int(d["dram_traffic_bytes"])
+    except (OSError, ValueError):
+        pass
+    return None
+
+
 def pct(x, q):
     return round(float(np.percentile(np.asarray(x, dtype=np.float64), q)), 2) if len(x) else None
 
@@ -283,7 +297,8 @@ def bench_c2(args):
                                "so it includes the wait behind earlier messages of the batch)"},
         "kernels_ms": {"put_avg": round(put_avg_ms, 5), "consume_avg": round(statistics.mean(get_ms), 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("ncu_put_c2.json"),
+                     "traffic_source": "profiles/ncu_put_c2.json (ncu --set full, put_kernel, same config)",
                      "kernel": "put_kernel", "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src_kind})",
                      "algorithmic_bytes_per_launch": put_bytes},
         "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": m * stride,
