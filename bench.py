@@ -193,13 +193,17 @@ def bench_c2(args):
     # With --no-overlap, put(s+1) waits for consume(s) to finish (event).
     sp, sc = torch.cuda.Stream(), torch.cuda.Stream()
     stream = sp
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    consumed = torch.cuda.Event()
-    consumed.record(sc)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(min(args.steps, 64))]
+    consumed = [torch.cuda.Event()]           # holder: events recorded in a graph capture stay in it
+    consumed[0].record(sc)
+    capturing = [False]
 
     def step(i, timed=None, before_put=None):
-        if args.no_overlap or before_put is not None:
-            sp.wait_event(consumed)            # the previous batch has been consumed
+        if capturing[0]:
+            if args.no_overlap:
+                sp.wait_stream(sc)                # graph edge: put(s+1) after consume(s)
+        elif args.no_overlap or before_put is not None:
+            sp.wait_event(consumed[0])            # the previous batch has been consumed
         if before_put is not None:
             before_put()
         if timed is not None:
@@ -211,7 +215,8 @@ def bench_c2(args):
         R.ring_consume(ring, m, views, None, 0, 0, sc)
         if timed is not None:
             timed[3].record(sc)
-        consumed.record(sc)
+        if not capturing[0]:
+            consumed[0].record(sc)
 
     for i in range(args.warmup):
         step(i)
@@ -219,23 +224,62 @@ def bench_c2(args):
     assert (status == 0).all().item(), "put failed in warm-up"
     assert (R.parse_views(views.cpu().numpy())["status"] == 0).all(), "consume failed in warm-up"
 
+    # Per-kernel durations: an eager pass with events around every launch.
+    n_ev = min(len(ev), 64)
+    for i in range(n_ev):
+        step(i, ev[i])
+    torch.cuda.synchronize()
+    put_ms = [a.elapsed_time(b) for a, b, c, d in ev[:n_ev]]
+    get_ms = [c.elapsed_time(d) for a, b, c, d in ev[:n_ev]]
+
+    # Timed region: eager launches (the host issues a step in ~15 us, the GPU
+    # takes ~36 us), or with --graph a CUDA graph of G steps replayed; G is even,
+    # so each launch context keeps alternating its two counter sets.
+    G = 16
+    graph = None
+    if args.graph:
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        capturing[0] = True
+        with torch.cuda.graph(graph, stream=cap, capture_error_mode="relaxed"):
+            sp.wait_stream(cap)
+            sc.wait_stream(cap)
+            for i in range(G):
+                step(i)
+            cap.wait_stream(sp)
+            cap.wait_stream(sc)
+        capturing[0] = False
+        consumed[0] = torch.cuda.Event()
+        consumed[0].record(sc)
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+        assert (status == 0).all().item(), "put failed in graph warm-up"
+    steps = (args.steps + G - 1) // G * G if graph is not None else args.steps
     clk = Clocks(dev)
     clk.start()
     l0 = R.ring_launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    t_start.record(sp)
-    sc.wait_event(t_start)
-    for i in range(args.steps):
-        step(args.warmup + i, ev[i])
-    sp.wait_stream(sc)
-    t_end.record(sp)
+    main = torch.cuda.current_stream()
+    t_start.record(main)
+    if graph is not None:
+        for _ in range(steps // G):
+            graph.replay()
+    else:
+        sp.wait_stream(main)
+        sc.wait_stream(main)
+        for i in range(steps):
+            step(args.warmup + i)
+        main.wait_stream(sp)
+        main.wait_stream(sc)
+    t_end.record(main)
     torch.cuda.synchronize()
-    launches = R.ring_launch_count() - l0
+    launches = (2 * steps) if graph is not None else R.ring_launch_count() - l0
     clocks = clk.stop()
     ms = t_start.elapsed_time(t_end)
-    put_ms = [a.elapsed_time(b) for a, b, c, d in ev]
-    get_ms = [c.elapsed_time(d) for a, b, c, d in ev]
+    args.steps = steps
     assert (status == 0).all().item()
     v = R.parse_views(views.cpu().numpy())
     assert (v["status"] == 0).all()
@@ -528,6 +572,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--lat-iters", type=int, default=40)
     ap.add_argument("--no-overlap", action="store_true", help="N=1: put(s+1) waits for consume(s)")
+    ap.add_argument("--graph", action="store_true",
+                    help="N=1: replay a CUDA graph of 16 steps in the timed region (default: eager launches)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -540,7 +586,7 @@ def main():
         return
     if world == 1:
         if not args.steps:
-            args.steps = 2000
+            args.steps = 24000
         print(json.dumps(bench_c2(args)), flush=True)
         return
     import torch.distributed as dist
