@@ -82,6 +82,13 @@ struct MsgBrief {        // the fields lane 0 needs, computed in parallel by all
 __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, LeaderState& L, uint32_t k0,
                                  uint32_t gmax, GroupSlot* gs, const MsgBrief* brief, const DestDesc* dests) {
   (void)k0;
+  // MPSC: the lock taken for the round's first message is kept for the
+  // following messages to the same ring and released after the round's last
+  // item (lock coarsening).  Equivalent to the oracle schedule in which the
+  // producer re-acquires the lock right after each Unlock.
+  int held = -1;
+  uint32_t done_l = gmax;
+  uint32_t last_pad = 0xffffffffu;
   for (uint32_t l = 0; l < gmax; ++l) {
     if (a.trace && k0 == 0 && l < 32) a.trace[128 + l] = globaltimer();
     const MsgBrief& m = brief[l];
@@ -102,7 +109,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
       }
     }
     const DestDesc D = dests[d];
-    if (D.mpsc && l > 0) return l;               // MPSC: one message per round (lock per append)
+    if (l > 0 && ((D.mpsc && held != (int)d) || (!D.mpsc && held >= 0))) { done_l = l; break; }
     o.dest = d;
     if (!(L.loaded & (1u << d))) {
       L.loaded |= 1u << d;
@@ -114,11 +121,11 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
     if (L.aborted) o.status = RING_ETIMEDOUT;
     else if (o.status == RING_OK && (m.len >= (1ull << 32) || f > D.R)) o.status = RING_EMSGSIZE;
 
-    bool locked = false;
+    bool locked = held == (int)d;
     uint64_t P = L.tails[d];
     // %globaltimer is read only when a wait starts (keeps the serial path lean).
-    uint64_t t_start = (o.status == RING_OK && D.mpsc) ? globaltimer() : 0;
-    if (o.status == RING_OK && D.mpsc) {
+    uint64_t t_start = (o.status == RING_OK && D.mpsc && !locked) ? globaltimer() : 0;
+    if (o.status == RING_OK && D.mpsc && !locked) {
       // Step 1 "Acquire the lock using a CAS-based spinlock",
       // after our own previous items (and their Unlock) are published.
       while (ld_acquire_gpu32(&S->pub_seq) != L.items)
@@ -147,8 +154,10 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
           P = pack_ptr(advance(ptr_off(P), w & kFMask, D.R), seq_inc(ptr_seq(P)));
           if (D.sys) st_release<true>(tail_w(D), P); else st_release<false>(tail_w(D), P);
         }
+        held = (int)d;
       }
     }
+    bool defer = false;
     // Step 3: space check (R4), PAD entry at the wrap (R3), credit wait (R12).
     if (o.status == RING_OK) {
       while (true) {
@@ -160,6 +169,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
           if (span_free(pb, pq, hb, hq, D.R - pb)) {
             const uint64_t P2 = pack_ptr(0, seq_inc(pq));
             write_pad_plan(ctx, L.items, d, pq, kBusy | kPad | (D.R - pb), P2);
+            last_pad = L.items;
             L.items++;
             P = P2;
             L.tails[d] = P;
@@ -180,11 +190,11 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         const uint64_t H2 = read_head(D);
         if (H2 != H) { L.heads[d] = H2; continue; }
         if (a.flags & RING_TRY) { o.status = RING_FULL; break; }   // "release the lock and abort"
-        if (l > 0 && !locked) {
+        if (l > 0) {
           // Hand what is decided (and any PAD just planned) to the copy
-          // warps and the publisher before waiting.
-          L.tails[d] = P;
-          return l;
+          // warps and the publisher (and release the lock) before waiting.
+          defer = true;
+          break;
         }
         // A PAD planned in this round must be published before waiting: the
         // consumer may have to free it for this message to fit (R3).
@@ -200,21 +210,27 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
       }
     }
     L.tails[d] = P;
+    if (defer) { done_l = l; break; }
     if (o.status == RING_ETIMEDOUT) L.aborted = true;
     if (hit >= 0) a.routes[hit].rr = a.routes[hit].rr + 1;   // committed: advance the round robin
     o.seq = (uint32_t)L.chans[d];
     L.chans[d] += 1;
     o.item = L.items++;
-    o.flags = kStatus | (o.status == RING_OK ? kEntry : 0u) | (locked ? kUnlock : 0u);
+    o.flags = kStatus | (o.status == RING_OK ? kEntry : 0u);
     if (o.status == RING_OK) {
       o.nunits = m.nunits;
       o.first_unit = L.units;
       L.units += o.nunits;
     }
     gs[l] = o;
-    if (locked) return l + 1;
   }
-  return gmax;
+  if (held >= 0) {
+    // Step 8 "Release the lock" after the round's LAST item (a PAD planned
+    // for a deferred message comes after the last message item).
+    if (last_pad == L.items - 1) ctx->plan[last_pad % kPlanRing].flags |= kUnlock;
+    else gs[done_l - 1].flags |= kUnlock;
+  }
+  return done_l;
 }
 
 // Warp-parallel placement of one round for a single SPSC destination (no
