@@ -159,7 +159,6 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
         p.src = reinterpret_cast<uint64_t>(a.data + start + kHdr);
         p.dst = reinterpret_cast<uint64_t>(a.dst + (uint64_t)mi * a.dst_stride);
         p.len = deliver ? len : 0;
-        p.hdr_dst = 0;
         p.nunits = nu;
         p.first_unit = units + nu_incl - nu;
         p.f = f;
@@ -210,7 +209,7 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
   if (lane == 0) {
     *g_cursor(a.ring) = G;
     if (pending) publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
-    if (copy) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&S->done), "r"(1u) : "memory");
+    if (copy) st_release<false>(&S->planned, make_planned(items, units) | kPlannedDone);
   }
 }
 
@@ -224,8 +223,9 @@ __device__ void get_finisher(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   while (true) {
     uint32_t ps = 0, done = 0;
     if (lane == 0) {
-      done = ld_acquire_gpu32(&S->done);   // before `planned`: final once done is seen
-      ps = planned_items(ld_acquire<false>(&S->planned));
+      const uint64_t pl = ld_acquire<false>(&S->planned);
+      ps = planned_items(pl);
+      done = planned_done(pl);
     }
     __syncwarp();
     ps = __shfl_sync(0xffffffffu, ps, 0);
@@ -275,8 +275,10 @@ __global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
   LaunchSet* S = &ctx->set[a.launch & 1];
   const int warp = threadIdx.x >> 5;
   __shared__ uint32_t s_crc[kCrcTableWords];
+  __shared__ CopyShared cs;
+  if (threadIdx.x == 0) { cs.pl = 0; cs.owner = 0; }
   if (blockIdx.x == 0) {
-    load_crc_table(s_crc, a.crc_table);
+    load_crc_table(s_crc, a.crc_table);   // (its __syncthreads also covers cs)
     if (warp == 0) {
       reset_set(&ctx->set[(a.launch + 1) & 1], threadIdx.x & 31);
       get_control<SYS>(a, ctx, S, s_crc);
@@ -287,7 +289,8 @@ __global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
       return;
     }
   }
-  if (a.dst) copy_warp(ctx, S, a.chunk, a.timeout_ns);
+  if (blockIdx.x != 0) __syncthreads();
+  if (a.dst) copy_warp(ctx, S, &cs, a.chunk, a.timeout_ns);
 }
 
 // In-order release of `count` received entries plus the PAD entries the read

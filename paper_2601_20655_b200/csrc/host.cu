@@ -121,7 +121,7 @@ ring_status_t enable_peer(int from, int to) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-constexpr uint32_t kTraceWords = 1280;   // debug timeline of one put launch
+constexpr uint32_t kTraceWords = 2048;   // debug timeline of one put launch
 
 }  // namespace
 
@@ -448,7 +448,11 @@ ring_status_t ring_peer_trace(ring_peer_t p, uint64_t* host_out, uint32_t n) {
   if (!p->trace) return RING_EINVAL;
   DevGuard g(p->device);
   CUDA_TRY(cudaDeviceSynchronize());
-  CUDA_TRY(cudaMemcpy(host_out, p->trace, 8ull * std::min<uint32_t>(n, kTraceWords), cudaMemcpyDeviceToHost));
+  // two halves (launch parity): the last launch first, then the one before it
+  const uint32_t last = (p->launches + 1) & 1;
+  const uint32_t n0 = std::min<uint32_t>(n, kTraceWords), n1 = std::min<uint32_t>(n - n0, kTraceWords);
+  CUDA_TRY(cudaMemcpy(host_out, p->trace + last * kTraceWords, 8ull * n0, cudaMemcpyDeviceToHost));
+  if (n1) CUDA_TRY(cudaMemcpy(host_out + n0, p->trace + (last ^ 1) * kTraceWords, 8ull * n1, cudaMemcpyDeviceToHost));
   return RING_OK;
 }
 
@@ -460,7 +464,13 @@ static void default_grid(int device, bool sys, uint32_t* ctas, uint32_t* threads
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
   if (!*ctas) *ctas = sys ? 33u : (uint32_t)nsm;
-  if (!*threads) *threads = 512;
+  // Local (HBM -> HBM): 8 warps per SM already keep ~10 MB in flight, enough
+  // for HBM (Little's law at ~1.5 us loaded latency); more warps only queue,
+  // every unit then completes at the very end of the launch and the consumer
+  // cannot release (and the next put cannot place) anything earlier.  With 8
+  // warps units complete in waves, in order, and the streaming C2 step is ~10%
+  // faster (profiles/r01_threads_sweep.txt).  NVLink (sys) needs more in flight.
+  if (!*threads) *threads = sys ? 512u : 256u;
   if (!*chunk) {
     *chunk = 32u << 10;
     // tuning knob (power of two, 4 KiB .. 1 MiB)
@@ -493,9 +503,12 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   a.chunk = chunk;
   a.launch = p->launches;
   if (getenv("B200RING_TRACE")) {
-    if (!p->trace) CUDA_TRY(cudaMalloc(&p->trace, kTraceWords * 8));
-    CUDA_TRY(cudaMemsetAsync(p->trace, 0, kTraceWords * 8, as_stream(stream)));
-    a.trace = p->trace;
+    if (!p->trace) {
+      CUDA_TRY(cudaMalloc(&p->trace, 2 * kTraceWords * 8));
+      CUDA_TRY(cudaMemset(p->trace, 0, 2 * kTraceWords * 8));
+    }
+    a.trace = p->trace + (p->launches & 1) * kTraceWords;
+    CUDA_TRY(cudaMemsetAsync(a.trace, 0, kTraceWords * 8, as_stream(stream)));
   }
   CUDA_TRY(launch_put(a, ctas, thr, as_stream(stream)));
   p->launches++;

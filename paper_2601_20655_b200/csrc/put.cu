@@ -8,11 +8,13 @@
 //     tail (SPSC: producer-local), GH stale-slot check (R6), space check with
 //     the interval rule (R4) against the cached head, PAD entry at the wrap
 //     (R3), waiting for credit only when nothing else is pending (R12).  Then
-//     every lane builds its message's 64-B header (R11) and CRC-32 (R10) and
-//     writes its plan; one release hands the round to the copy warps.
-//   copy warps (step 5, WB): header + payload into the (peer) ring.
-//   publisher (steps 6-8): lanes check 32 consecutive items at once; for the
-//     leading run of complete items they write the size slots busy|f (WL),
+//     every lane writes its placement; one release hands the round's copies
+//     out, then the lanes build the 64-B headers (R11) and CRC-32 (R10) into
+//     the plans while the copies run (a second release, `hdr_seq`).
+//   copy warps (step 5, WB): payload into the (peer) ring.
+//   publisher (steps 5-8): lanes check 32 consecutive items at once; for the
+//     leading run of complete items they write the headers (WB) and the size
+//     slots busy|f (WL),
 //     then lane 0 moves the tail with ONE system-scope release (UH) and, MPSC,
 //     releases the lock (Unlock).  The fence (MEMBAR.SYS, ~1.7 us on B200) is
 //     thus paid once per run of entries, and overlaps later copies.
@@ -63,7 +65,7 @@ struct LeaderState {
 __device__ __forceinline__ void write_pad_plan(LaunchCtx* ctx, uint32_t item, uint32_t dest, uint32_t slot,
                                                uint64_t word, uint64_t tail_after) {
   Plan& p = ctx->plan[item % kPlanRing];
-  p.len = 0; p.hdr_dst = 0; p.nunits = 0; p.first_unit = 0;
+  p.len = 0; p.nunits = 0; p.first_unit = 0;
   p.slot_word = word; p.slot = slot; p.tail_after = tail_after; p.dest = dest;
   p.flags = kEntry; p.status = RING_OK; p.msg = 0;
 }
@@ -313,7 +315,7 @@ __device__ uint32_t fast_place(const PutArgs& a, LaunchCtx* ctx, LeaderState& L,
   return run;
 }
 
-__device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const uint32_t* crc_tab) {
+__device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   const int lane = threadIdx.x & 31;
   __shared__ GroupSlot gs[kGroup];
   __shared__ MsgBrief brief[kGroup];
@@ -342,7 +344,8 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
     __syncwarp();
     if (lane == 0) {
       // Flow control: the round adds at most 2 items per message.
-      if (L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing) {
+      if (L.items + 2 * gmax > (uint32_t)kPlanRing &&
+          L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing) {
         const uint64_t end = globaltimer() + 2 * a.timeout_ns;
         while (L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing)
           if (globaltimer() > end) { L.aborted = true; break; }
@@ -367,11 +370,10 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
       __syncwarp();
       g = s_g;
     }
-    if (lane == 0 && a.trace && k0 / kGroup < 64) a.trace[(k0 / kGroup) * 4 + 1] = globaltimer();
+    // placements: one release hands the round's copies (and headers) out
+    const uint32_t k = k0 + lane;
+    const GroupSlot o = gs[lane & 31];
     if ((uint32_t)lane < g) {
-      const uint32_t k = k0 + lane;
-      const ring_msg_t m = a.msgs ? a.msgs[k] : a.inline_msg;
-      const GroupSlot o = gs[lane];
       Plan& p = ctx->plan[o.item % kPlanRing];
       p.msg = k;
       p.status = o.status;
@@ -380,54 +382,35 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
       p.nunits = o.nunits;
       p.first_unit = o.first_unit;
       p.len = 0;
-      p.hdr_dst = 0;
       if (o.status == RING_OK) {
+        const ring_msg_t* mp = a.msgs ? a.msgs + k : &a.inline_msg;
         const DestDesc& D = s_dests[o.dest];
-        const uint64_t f = footprint(m.len);
-        // ---- entry header (R11) + CRC-32 over bytes [4, 56) (R10)
-        uint32_t w[16];
-        const uint32_t* uid = reinterpret_cast<const uint32_t*>(m.hdr.uid);
-        const uint32_t len32 = (uint32_t)m.len;
-        w[1] = uid[0]; w[2] = uid[1]; w[3] = uid[2]; w[4] = uid[3];
-        w[5] = (uint32_t)m.hdr.accepted_at;
-        w[6] = (uint32_t)(m.hdr.accepted_at >> 32);
-        w[7] = m.hdr.app_id;
-        w[8] = (uint32_t)m.hdr.stage | (len32 << 16);   // stage[32,34) payload_len[34,36)
-        w[9] = len32 >> 16;                             // payload_len[36,38) reserved[38,40)
-        w[10] = 0;                                      // reserved[40,44)
-        w[11] = D.producer_id;
-        w[12] = o.seq;
-        w[13] = o.epoch & 0xffffu;                      // epoch[52,54) flags[54,56)
-        w[0] = crc52(w, crc_tab);
-        const uint64_t t = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();
-        w[14] = (uint32_t)t;
-        w[15] = (uint32_t)(t >> 32);
-        int4* ph = reinterpret_cast<int4*>(p.hdr);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ph[q] = make_int4((int)w[4 * q], (int)w[4 * q + 1], (int)w[4 * q + 2], (int)w[4 * q + 3]);
-        p.src = m.src;
+        const uint64_t len = brief[lane].len;
+        const uint64_t f = brief[lane].f;
+        p.src = mp->src;
         p.dst = reinterpret_cast<uint64_t>(D.data + o.start + kHdr);
-        p.len = m.len;
-        p.hdr_dst = reinterpret_cast<uint64_t>(D.data + o.start);
+        p.len = len;
+        p.start = o.start;
         p.slot = o.slot;
         p.slot_word = kBusy | f;
         p.tail_after = o.tail_after;
         p.f = f;
+        p.seq = o.seq;
+        p.epoch = o.epoch;
       }
+      S->arrive[o.item % kPlanRing] = 0;   // item o.item - kPlanRing is published (flow control)
       if (a.dest_out) a.dest_out[k] = o.dest;
     }
     __syncwarp();
     if (lane == 0) {
-      // One release hands the whole round (all lanes' plans, any PAD plans)
-      // to the copy warps and the publisher.
       st_release<false>(&S->planned, make_planned(L.items, L.units));
       const uint32_t rnd = k0 / kGroup;
-      if (a.trace && rnd < 64) { a.trace[rnd * 4 + 2] = globaltimer(); a.trace[rnd * 4 + 3] = g; }
+      if (a.trace && rnd < 64) { a.trace[rnd * 4 + 1] = globaltimer(); a.trace[rnd * 4 + 3] = g; }
     }
     k0 += g;
   }
   if (lane == 0) {
-    st_u32_release_gpu(&S->done, 1u);
+    st_release<false>(&S->planned, make_planned(L.items, L.units) | kPlannedDone);
     for (uint32_t d = 0; d < kMaxRouterDests && d < a.n_dests; ++d)
       if (L.loaded & (1u << d)) {
         a.dests[d].st->chan_seq = L.chans[d];
@@ -436,42 +419,113 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const
   }
 }
 
-// Steps 6-8 (WL, UH, Unlock), 32 items per look, in item order.  Lane l
-// caches the plan of item i + l (read once); each look only polls the arrive
-// counters.  For the leading run of complete items: the lanes write the size
-// slots (WL), ONE fence orders the payload copies (observed through the
-// arrive counters) and the slots before the tail store (UH) and pub_seq.
-__device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
+// Entry header (R11) + CRC-32 over bytes [4, 56) (R10) of plan item j,
+// written to the ring together with the item's status and, for an SPSC ring,
+// its size slot (WL).  SPSC: no reader looks at a slot past the tail (the
+// stale-slot check GH runs under the MPSC lock only, R6), so the slot can be
+// written before the payload is complete; the fence before the tail store
+// still orders it, and nothing is left for that fence to wait for.
+__device__ __forceinline__ void write_header(const PutArgs& a, LaunchCtx* ctx, uint32_t j, const uint32_t* crc_tab) {
+  const Plan& p = ctx->plan[j % kPlanRing];
+  const uint32_t flags = ld_cg32(&p.flags), status = ld_cg32(&p.status), msg = ld_cg32(&p.msg);
+  if (flags & kStatus) a.status[msg] = status;
+  if (!(flags & kEntry)) return;
+  const DestDesc& D = a.dests[ld_cg32(&p.dest)];
+  if ((flags & kStatus) && status == RING_OK) {
+    const ring_msg_t* mp = a.msgs ? a.msgs + msg : &a.inline_msg;
+    const uint32_t* uid = reinterpret_cast<const uint32_t*>(mp->hdr.uid);   // (4-B aligned in kernel params)
+    const uint4 u0 = make_uint4(uid[0], uid[1], uid[2], uid[3]);
+    const uint64_t acc = mp->hdr.accepted_at;
+    const uint32_t app = mp->hdr.app_id, stage = mp->hdr.stage;
+    const uint32_t len32 = (uint32_t)ld_cg64(&p.len);
+    uint32_t w[16];
+    w[1] = u0.x; w[2] = u0.y; w[3] = u0.z; w[4] = u0.w;
+    w[5] = (uint32_t)acc;
+    w[6] = (uint32_t)(acc >> 32);
+    w[7] = app;
+    w[8] = stage | (len32 << 16);          // stage[32,34) payload_len[34,36)
+    w[9] = len32 >> 16;                    // payload_len[36,38) reserved[38,40)
+    w[10] = 0;                             // reserved[40,44)
+    w[11] = D.producer_id;
+    w[12] = ld_cg32(&p.seq);
+    w[13] = ld_cg32(&p.epoch) & 0xffffu;   // epoch[52,54) flags[54,56)
+    w[0] = crc52(w, crc_tab);
+    const uint64_t t = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();
+    w[14] = (uint32_t)t;
+    w[15] = (uint32_t)(t >> 32);
+    uint8_t* hd = D.data + ld_cg64(&p.start);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st16(hd + 16 * q, make_int4((int)w[4 * q], (int)w[4 * q + 1], (int)w[4 * q + 2], (int)w[4 * q + 3]));
+  }
+  if (!D.mpsc) {   // WL (SPSC, early; PAD entries carry the pad bit)
+    if (D.sys) st_relaxed<true>(slot_w(D, ld_cg32(&p.slot)), ld_cg64(&p.slot_word));
+    else st_relaxed<false>(slot_w(D, ld_cg32(&p.slot)), ld_cg64(&p.slot_word));
+  }
+}
+
+// Steps 5-8 (WB header, WL, UH, Unlock), in item order.  As soon as items are
+// planned the lanes write their headers (write_header), off the copy critical
+// path.  For publication lane l caches the plan of item i + l (read once);
+// each look only polls the arrive counters.  For the leading run of complete
+// items the lanes write the size slots (WL, MPSC rings).  Runs accumulate
+// while whole windows keep completing; then ONE fence orders the payload
+// copies (observed through the arrive counters), headers and slots before the
+// tail store (UH), the Unlock and pub_seq.  A flush happens at a partial
+// window, at an Unlock, at a change of destination and whenever nothing more
+// is complete.
+__device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, const uint32_t* crc_tab) {
   const int lane = threadIdx.x & 31;
-  uint32_t i = 0, trace_n = 0, ps = 0, done = 0;
+  uint32_t i = 0, trace_n = 0, ps = 0, hq = 0;
+  bool done = false;
   uint64_t idle_since = 0;
   bool have = false;
-  uint32_t flags = 0, dest = 0, nunits = 0, slot = 0, msg = 0, status = 0;
+  uint32_t flags = 0, dest = 0, nunits = 0, slot = 0;
   uint64_t slot_word = 0, tail_after = 0;
+  // accumulated, not yet fenced: destination, tail, Unlock
+  bool pend = false, pend_entries = false, pend_unlock = false;
+  uint32_t pend_dest = 0, pend_n = 0;
+  uint64_t pend_tail = 0;
   if (a.trace && lane == 0) a.trace[255] = globaltimer();
+  auto flush = [&]() {
+    const DestDesc& D = a.dests[pend_dest];
+    // acquire for the arrive counters read before, release for the copies, headers and slots
+    if (D.sys) fence_acq_rel<true>(); else fence_acq_rel<false>();
+    if (lane == 0) {
+      if (pend_entries) {   // UH
+        if (D.sys) st_relaxed<true>(tail_w(D), pend_tail); else st_relaxed<false>(tail_w(D), pend_tail);
+      }
+      if (pend_unlock) {    // Unlock after the tail
+        if (D.sys) st_release<true>(lock_w(D), 0ull); else st_release<false>(lock_w(D), 0ull);
+      }
+      st_u32_relaxed_gpu(&S->pub_seq, i);   // ordered by the fence
+      if (a.trace && trace_n < 512) {
+        a.trace[256 + 2 * trace_n] = globaltimer();
+        a.trace[257 + 2 * trace_n] = i;
+      }
+    }
+    trace_n++;
+    pend = pend_entries = pend_unlock = false;
+    pend_n = 0;
+  };
   while (true) {
     const uint32_t j = i + lane;
-    // Independent loads in one pass: lane 0 looks for newly planned items (relaxed),
-    // every lane with a cached item polls its arrive counter (relaxed).
+    // Independent loads in one pass: lane 0 looks for newly planned items
+    // (relaxed), every lane with a cached item polls its arrive counter.
     uint64_t pl = 0;
-    uint32_t dn = 0, arr = 0;
-    if (lane == 0 && !done) {
-      dn = ld_relaxed_gpu32(&S->done);
-      pl = ld_relaxed<false>(&S->planned);
-    }
+    uint32_t arr = 0;
+    if (lane == 0 && !done) pl = ld_relaxed<false>(&S->planned);
     if (have && nunits) arr = ld_relaxed_gpu32(&S->arrive[j % kPlanRing]);
-    dn = __shfl_sync(0xffffffffu, dn, 0);
     pl = __shfl_sync(0xffffffffu, pl, 0);
-    if (!done && (dn || planned_items(pl) != ps)) {
-      // acquire the newer plans (done is released after the final `planned`)
-      uint32_t p = 0;
-      if (lane == 0) {
-        if (dn) (void)ld_acquire_gpu32(&S->done);
-        p = planned_items(ld_acquire<false>(&S->planned));
-      }
-      __syncwarp();
-      ps = __shfl_sync(0xffffffffu, p, 0);
-      done = dn;
+    if (!done && (planned_done(pl) || planned_items(pl) != ps)) {
+      uint64_t p = 0;
+      if (lane == 0) p = ld_acquire<false>(&S->planned);   // acquire the newer plans
+      p = __shfl_sync(0xffffffffu, p, 0);
+      ps = planned_items(p);
+      done = planned_done(p);
+      // headers of the newly planned items
+      for (; hq < ps; hq += 32)
+        if (hq + lane < ps) write_header(a, ctx, hq + lane, crc_tab);
+      hq = ps;
     }
     if (i >= ps && done) break;
     if (!have && j < ps) {
@@ -480,8 +534,6 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
       dest = ld_cg32(&p.dest);
       nunits = ld_cg32(&p.nunits);
       slot = ld_cg32(&p.slot);
-      msg = ld_cg32(&p.msg);
-      status = ld_cg32(&p.status);
       slot_word = ld_cg64(&p.slot_word);
       tail_after = ld_cg64(&p.tail_after);
       have = true;
@@ -490,6 +542,7 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     const bool ready = have && (nunits == 0 || arr == nunits);
     const uint32_t notready = __ballot_sync(0xffffffffu, !ready);
     uint32_t run = notready ? __ffs(notready) - 1 : 32;
+    const bool full = run == 32;
     // a run stays on one destination and ends at an Unlock
     const uint32_t dest0 = __shfl_sync(0xffffffffu, dest, 0);
     const uint32_t other = __ballot_sync(0xffffffffu, (uint32_t)lane < run && dest != dest0);
@@ -497,39 +550,31 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     const uint32_t unl = __ballot_sync(0xffffffffu, (uint32_t)lane < run && (flags & kUnlock));
     if (unl) run = min(run, (uint32_t)__ffs(unl));
     if (run == 0) {
+      if (pend) { flush(); continue; }
       const uint64_t t = globaltimer();
       if (!idle_since) idle_since = t;
       else if (t - idle_since > 2 * a.timeout_ns) break;
       continue;
     }
     idle_since = 0;
+    if (pend && dest0 != pend_dest) flush();
     const DestDesc& D = a.dests[dest0];
     const bool mine = (uint32_t)lane < run;
-    if (mine && nunits) S->arrive[j % kPlanRing] = 0;
-    if (mine && (flags & kEntry)) {   // WL: size + busy bit (PAD entries carry the pad bit)
+    if (mine && (flags & kEntry) && D.mpsc) {   // WL: size + busy bit (PAD entries carry the pad bit)
       if (D.sys) st_relaxed<true>(slot_w(D, slot), slot_word);
       else st_relaxed<false>(slot_w(D, slot), slot_word);
     }
     const uint32_t entries = __ballot_sync(0xffffffffu, mine && (flags & kEntry));
-    const uint64_t tail = __shfl_sync(0xffffffffu, tail_after, entries ? 31 - __clz(entries) : 0);
-    // acquire for the arrive counters read above, release for the copies and slots
-    if (D.sys) fence_acq_rel<true>(); else fence_acq_rel<false>();
-    if (lane == 0) {
-      if (entries) {   // UH: one fence covers the run's entries
-        if (D.sys) st_relaxed<true>(tail_w(D), tail); else st_relaxed<false>(tail_w(D), tail);
-      }
-      if (unl && (uint32_t)__ffs(unl) == run) {   // Unlock after the tail
-        if (D.sys) st_release<true>(lock_w(D), 0ull); else st_release<false>(lock_w(D), 0ull);
-      }
+    if (entries) {
+      pend_tail = __shfl_sync(0xffffffffu, tail_after, 31 - __clz(entries));
+      pend_entries = true;
     }
-    if (mine && (flags & kStatus)) a.status[msg] = status;
-    if (a.trace && lane == 0 && trace_n < 512) {
-      a.trace[256 + 2 * trace_n] = globaltimer();
-      a.trace[257 + 2 * trace_n] = ((uint64_t)i << 16) | run;
-      trace_n++;
-    }
+    pend = true;
+    pend_dest = dest0;
+    pend_n += run;
+    const bool unlock_now = unl && (uint32_t)__ffs(unl) == run;
+    pend_unlock = unlock_now;
     i += run;
-    if (lane == 0) st_u32_relaxed_gpu(&S->pub_seq, i);
     // slide the window by `run`
     const uint32_t src = min((uint32_t)lane + run, 31u);
     const bool h2 = __shfl_sync(0xffffffffu, have, src) && (uint32_t)lane + run < 32;
@@ -537,12 +582,13 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     dest = __shfl_sync(0xffffffffu, dest, src);
     nunits = __shfl_sync(0xffffffffu, nunits, src);
     slot = __shfl_sync(0xffffffffu, slot, src);
-    msg = __shfl_sync(0xffffffffu, msg, src);
-    status = __shfl_sync(0xffffffffu, status, src);
     slot_word = __shfl_sync(0xffffffffu, slot_word, src);
     tail_after = __shfl_sync(0xffffffffu, tail_after, src);
     have = h2;
+    // keep accumulating only while whole windows complete
+    if (!full || unlock_now || run < 32 || pend_n >= 96) flush();
   }
+  if (pend) flush();
 }
 
 __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
@@ -550,15 +596,22 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
   LaunchSet* S = &ctx->set[a.launch & 1];
   const int warp = threadIdx.x >> 5;
   __shared__ uint32_t s_crc[kCrcTableWords];
+  __shared__ CopyShared cs;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) { cs.pl = 0; cs.owner = 0; }
+  __syncthreads();
   if (blockIdx.x == 0) {
-    load_crc_table(s_crc, a.crc_table);
+    if (a.trace && threadIdx.x == 0) a.trace[252] = globaltimer();
     if (warp == 0) {
-      reset_set(&ctx->set[(a.launch + 1) & 1], threadIdx.x & 31);
-      put_leader(a, ctx, S, s_crc);
+      reset_set(&ctx->set[(a.launch + 1) & 1], lane);
+      put_leader(a, ctx, S);
       return;
     }
-    if (warp == 1) {
-      put_publisher(a, ctx, S);
+    if (warp == 1) {   // the publisher writes the headers: it holds the CRC tables
+      for (int i = lane; i < kCrcTableWords; i += 32) s_crc[i] = a.crc_table[i];
+      __syncwarp();
+      put_publisher(a, ctx, S, s_crc);
+      if (a.trace && lane == 0) a.trace[253] = globaltimer();
       return;
     }
   }
@@ -567,7 +620,7 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
     if (warp == (blockIdx.x == 0 ? 2 : 0)) copy_engine<kEngineStages>(ctx, S, a.chunk, a.timeout_ns, dyn_smem);
     return;
   }
-  copy_warp(ctx, S, a.chunk, a.timeout_ns);
+  copy_warp(ctx, S, &cs, a.chunk, a.timeout_ns, a.trace);
 }
 
 // With CUDA's lazy module loading, the first launch of a kernel loads it, and

@@ -57,7 +57,39 @@ __device__ __forceinline__ void reset_set(LaunchSet* s, int lane) {
     s->planned = 0;
     s->pub_seq = 0;
     s->next_unit = 0;
-    s->done = 0;
+  }
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_cta_shared64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_shared64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.cta.shared::cta.u64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "l"(v) : "memory");
+}
+
+// Lane 0: wait until unit u is planned (returns the `planned` word that covers
+// it) or the launch has no unit u (returns a done word with fewer units).
+// Causality: control warp release -> (gpu acquire) poller -> (cta release /
+// acquire through shared memory) this warp; the plan loads that follow are
+// ordered after it (PTX causality order is transitive across scopes).
+__device__ __forceinline__ uint64_t wait_planned(LaunchSet* S, CopyShared* cs, uint32_t u, uint64_t timeout_ns,
+                                                 bool& timed_out) {
+  uint64_t end = 0;
+  while (true) {
+    const uint64_t v = ld_acquire_cta_shared64(&cs->pl);
+    if (planned_units(v) > u || planned_done(v)) return v;
+    if (atomicCAS_block(&cs->owner, 0u, 1u) == 0u) {
+      const uint64_t g = ld_acquire<false>(&S->planned);
+      if (g != v) st_release_cta_shared64(&cs->pl, g);   // monotonic: one poller at a time
+      atomicExch_block(&cs->owner, 0u);
+      if (planned_units(g) > u || planned_done(g)) return g;
+    }
+    const uint64_t t = globaltimer();
+    if (!end) end = t + 2 * timeout_ns;
+    else if (t > end) { timed_out = true; return v; }
+    __nanosleep(64);
   }
 }
 
@@ -66,32 +98,31 @@ __device__ __forceinline__ void reset_set(LaunchSet* s, int lane) {
 // launch makes progress even if some of its CTAs cannot be scheduled (other
 // kernels occupying SMs): the kernel never needs all its CTAs co-resident.
 // Returns when the control warp is done and every unit has been handed out, or
-// after `2 * timeout_ns` without progress.
-__device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns) {
+// after `2 * timeout_ns` without progress.  `cs` must be zeroed (and the CTA
+// synchronised) before the first call.
+//
+// After the control warp's release: one poller per CTA acquires it, then the
+// lanes read 32 candidate plans' copy sectors (unit range AND copy fields) in
+// one round trip; the hit lane broadcasts its fields.
+__device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShared* cs, uint32_t chunk,
+                                          uint64_t timeout_ns, uint64_t* trace = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t cur = 0;   // items before `cur` hold no unit this warp can still take
+  // debug timeline: the first unit of the first copy warp of each CTA
+  uint64_t* tr = (trace && (threadIdx.x >> 5) == (blockIdx.x == 0 ? 2 : 0)) ? trace + 1280 + 4 * blockIdx.x : nullptr;
   while (true) {
     uint32_t u = 0, quit = 0, ps = 0;
     if (lane == 0) {
+      if (tr) tr[0] = globaltimer();
       u = atomicAdd(&S->next_unit, 1u);
-      uint64_t end = 0;
-      // Poll with relaxed loads (no L1 invalidation per poll; thousands of
-      // warps may wait here), then one acquire once the unit is planned.
-      while (true) {
-        if (planned_units(ld_relaxed<false>(&S->planned)) > u) break;
-        if (ld_relaxed_gpu32(&S->done)) {
-          (void)ld_acquire_gpu32(&S->done);     // `planned` is final once done is seen
-          if (planned_units(ld_acquire<false>(&S->planned)) > u) break;
-          quit = 1;
-          break;
-        }
-        const uint64_t t = globaltimer();
-        if (!end) end = t + 2 * timeout_ns;
-        else if (t > end) { quit = 1; break; }
-        __nanosleep(64);
+      bool to = false;
+      const uint64_t pl = wait_planned(S, cs, u, timeout_ns, to);
+      if (to || planned_units(pl) <= u) {
+        quit = 1;
+        if (trace) atomicMax(reinterpret_cast<unsigned long long*>(trace + 254), (unsigned long long)globaltimer());
       }
-      // one acquire of the word that covered u: its items include u's item
-      ps = planned_items(ld_acquire<false>(&S->planned));
+      ps = planned_items(pl);
+      if (tr) tr[1] = globaltimer();
     }
     __syncwarp();
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -99,34 +130,41 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, uint32_t
     u = __shfl_sync(0xffffffffu, u, 0);
     ps = __shfl_sync(0xffffffffu, ps, 0);
     // find the item holding unit u (plans are read through L2: ring slots are reused)
-    uint32_t item = 0xffffffffu;
-    for (uint32_t b = cur; b < ps && item == 0xffffffffu; b += 32) {
+    uint32_t item = 0xffffffffu, fu = 0;
+    uint64_t src = 0, dst = 0, len = 0;
+    for (uint32_t b = cur; b < ps; b += 32) {
       const uint32_t i = b + lane;
       bool hit = false;
+      ulonglong2 q0 = make_ulonglong2(0, 0), q1 = make_ulonglong2(0, 0);
       if (i < ps) {
-        const Plan& p = ctx->plan[i % kPlanRing];
-        const uint32_t nu = ld_cg32(&p.nunits);
-        const uint32_t fu = ld_cg32(&p.first_unit);
-        hit = nu && u >= fu && u - fu < nu;
+        const ulonglong2* p = reinterpret_cast<const ulonglong2*>(&ctx->plan[i % kPlanRing]);
+        q0 = __ldcg(p);        // src, dst
+        q1 = __ldcg(p + 1);    // len, first_unit | nunits << 32
+        const uint32_t f0 = (uint32_t)q1.y, nu = (uint32_t)(q1.y >> 32);
+        hit = nu && u >= f0 && u - f0 < nu;
       }
       const uint32_t m = __ballot_sync(0xffffffffu, hit);
-      if (m) item = b + __ffs(m) - 1;
+      if (m) {
+        const int h = __ffs(m) - 1;
+        item = b + h;
+        src = __shfl_sync(0xffffffffu, q0.x, h);
+        dst = __shfl_sync(0xffffffffu, q0.y, h);
+        len = __shfl_sync(0xffffffffu, q1.x, h);
+        fu = (uint32_t)__shfl_sync(0xffffffffu, q1.y, h);
+        break;
+      }
     }
     if (item == 0xffffffffu) return;   // cannot happen with a consistent plan
     cur = item;
-    const Plan& p = ctx->plan[item % kPlanRing];
-    const uint64_t src = ld_cg64(&p.src), dst = ld_cg64(&p.dst), len = ld_cg64(&p.len);
-    const uint64_t hdr_dst = ld_cg64(&p.hdr_dst);
-    const uint32_t c = u - ld_cg32(&p.first_unit);
+    const uint32_t c = u - fu;
     const uint64_t lo = (uint64_t)c * chunk;
     const uint64_t hi = min(len, lo + chunk);
-    if (c == 0 && hdr_dst && lane < 4) {
-      const int4 h = __ldcg(reinterpret_cast<const int4*>(p.hdr) + lane);
-      st16(reinterpret_cast<uint8_t*>(hdr_dst) + 16 * lane, h);
-    }
+    if (tr && lane == 0) tr[2] = globaltimer();
     if (hi > lo) warp_copy(reinterpret_cast<const uint8_t*>(src) + lo, reinterpret_cast<uint8_t*>(dst) + lo, hi - lo, lane);
     __syncwarp();
     if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);
+    if (tr && lane == 0) tr[3] = globaltimer();
+    tr = nullptr;
   }
 }
 
@@ -188,14 +226,9 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
       if (lane == 0) {
         if (pending_u == 0xffffffffu) pending_u = atomicAdd(&S->next_unit, 1u);
         u = pending_u;
-        if (planned_units(ld_relaxed<false>(&S->planned)) <= u) {
-          state = 1;
-          if (ld_relaxed_gpu32(&S->done)) {
-            (void)ld_acquire_gpu32(&S->done);
-            if (planned_units(ld_acquire<false>(&S->planned)) <= u) state = 2;
-          }
-        }
-        if (state == 0) ps = planned_items(ld_acquire<false>(&S->planned));
+        const uint64_t pl = ld_acquire<false>(&S->planned);
+        if (planned_units(pl) <= u) state = planned_done(pl) ? 2 : 1;
+        else ps = planned_items(pl);
       }
       __syncwarp();
       state = __shfl_sync(0xffffffffu, state, 0);
@@ -217,16 +250,11 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
       cur = item;
       const Plan& p = ctx->plan[item % kPlanRing];
       const uint64_t src = ld_cg64(&p.src), dst = ld_cg64(&p.dst), len = ld_cg64(&p.len);
-      const uint64_t hdr_dst = ld_cg64(&p.hdr_dst);
       const uint32_t c = u - ld_cg32(&p.first_unit);
       const uint64_t lo = (uint64_t)c * chunk;
       const uint64_t hi = min(len, lo + chunk);
       const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src) + lo;
       uint8_t* d8 = reinterpret_cast<uint8_t*>(dst) + lo;
-      if (c == 0 && hdr_dst && lane < 4) {
-        const int4 h = __ldcg(reinterpret_cast<const int4*>(p.hdr) + lane);
-        st16(reinterpret_cast<uint8_t*>(hdr_dst) + 16 * lane, h);
-      }
       const uint64_t n = hi > lo ? hi - lo : 0;
       const bool aligned = ((((uintptr_t)s8) | ((uintptr_t)d8)) & 15) == 0;
       const uint32_t n16 = aligned ? (uint32_t)(n & ~15ull) : 0u;
@@ -236,7 +264,7 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
         if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);
         continue;
       }
-      __syncwarp();     // header / tail stores of the lanes precede the arrive issued later by lane 0
+      __syncwarp();     // tail stores of the lanes precede the arrive issued later by lane 0
       if (lane == 0) {
         const int s = (int)(k_issue % STAGES);
         st[s].dst = reinterpret_cast<uint64_t>(d8);
@@ -296,8 +324,8 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
 }
 
 __device__ __forceinline__ uint32_t units_for(uint64_t len, uint32_t chunk) {
-  const uint64_t u = (len + chunk - 1) >> (__ffs(chunk) - 1);
-  return u ? (uint32_t)u : 1u;   // at least one: it also writes the header
+  // an empty payload has no unit: entry headers are written by the put's publisher
+  return (uint32_t)((len + chunk - 1) >> (__ffs(chunk) - 1));
 }
 
 // Load the CRC slicing tables into shared memory (whole CTA participates).

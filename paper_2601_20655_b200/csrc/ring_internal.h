@@ -1,6 +1,7 @@
 // ring_internal.h — structures shared by the host runtime (host.cu) and the
 // kernels (put.cu, get.cu).  Not part of the public ABI.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -50,16 +51,30 @@ enum PlanFlags : uint32_t {
 // record (message not placed).  Written by the control warp, read by the copy
 // warps and the publisher / finisher warp.  192 bytes.
 struct alignas(64) Plan {
-  uint64_t src, dst, len, hdr_dst;  // copy: payload source / destination / bytes; header destination (0 = none)
+  // what a copy warp needs, in the first 32-B sector (one vector load pair per lane)
+  uint64_t src, dst, len;           // copy: payload source / destination / bytes
+  uint32_t first_unit, nunits;      // copy work units [first_unit, first_unit + nunits)
   uint64_t slot_word;               // busy | pad | f
   uint64_t tail_after;              // tail word once this entry is published (put)
   uint32_t slot, dest, msg, status; // slot seq; destination index; message index in the launch; status
-  uint32_t flags, first_unit, nunits, _q;
+  uint32_t flags, seq, epoch, _q;   // put: header seq (R18) and epoch of a message entry
   uint64_t f;
-  uint64_t _p[5];
-  uint32_t hdr[16];                 // the 64-B entry header (put)
+  uint64_t start;                   // put: entry offset in the data region (header goes to data + start)
+  uint64_t _p[4];
+  uint32_t _h[16];
 };
 static_assert(sizeof(Plan) == 192, "Plan layout");
+static_assert(offsetof(Plan, nunits) == 28, "copy fields in the first sector");
+
+// Per-CTA cache of the launch's `planned` word for the copy warps: one warp
+// at a time polls the global word (gpu-scope acquire) and republishes it in
+// shared memory (cta-scope release), so ~one poller per SM instead of one per
+// warp hits that L2 line.
+struct CopyShared {
+  uint64_t pl;
+  uint32_t owner;
+  uint32_t _p;
+};
 
 // Per-launch counters.  A context holds two sets used by alternate launches;
 // launch L uses set[L & 1] and zeroes set[(L + 1) & 1] for launch L + 1 (the
@@ -75,11 +90,13 @@ struct alignas(128) LaunchSet {
   uint32_t _b[31];
   uint32_t next_unit;      // copy work units handed out (atomic)
   uint32_t _c[31];
-  uint32_t done;           // control warp finished: `planned` is final (release)
-  uint32_t _d[31];
+  uint32_t _d[32];
   uint32_t arrive[kPlanRing];
 };
-__host__ __device__ inline uint32_t planned_items(uint64_t p) { return (uint32_t)p; }
+// Bit 31 of the items field: the control warp is done, the word is final.
+constexpr uint64_t kPlannedDone = 1ull << 31;
+__host__ __device__ inline uint32_t planned_items(uint64_t p) { return (uint32_t)p & 0x7fffffffu; }
+__host__ __device__ inline bool planned_done(uint64_t p) { return (p & kPlannedDone) != 0; }
 __host__ __device__ inline uint32_t planned_units(uint64_t p) { return (uint32_t)(p >> 32); }
 __host__ __device__ inline uint64_t make_planned(uint32_t items, uint32_t units) {
   return ((uint64_t)units << 32) | items;

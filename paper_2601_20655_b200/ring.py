@@ -193,8 +193,9 @@ def ring_peer_submitted(peer: int) -> int:
     return int(lib.ring_peer_submitted(peer))
 
 
-def ring_peer_trace(peer: int, n: int = 1280) -> np.ndarray:
-    """Debug timeline of the last put launch (needs B200RING_TRACE=1)."""
+def ring_peer_trace(peer: int, n: int = 4096) -> np.ndarray:
+    """Debug timelines (needs B200RING_TRACE=1): words [0, 2048) the last put
+    launch, [2048, 4096) the launch before it."""
     out = np.zeros(n, dtype=np.uint64)
     _check("ring_peer_trace", lib.ring_peer_trace(peer, out.ctypes.data, n))
     return out
