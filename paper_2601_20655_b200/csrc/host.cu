@@ -490,6 +490,7 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   a.status = d_status;
   a.ctx = p->ctx;
   a.dests = p->desc_dev;
+  a.dest0 = p->desc;
   a.n_dests = 1;
   a.crc_table = p->crc;
   a.timeout_ns = g_timeout_ns;
@@ -715,6 +716,7 @@ ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, 
   a.dest_out = d_dest;
   a.ctx = r->ctx;
   a.dests = r->dests_dev;
+  a.dest0 = r->dests[0]->desc;
   a.n_dests = (uint32_t)r->dests.size();
   a.routes = r->routes_dev;
   a.n_routes = r->max_routes;

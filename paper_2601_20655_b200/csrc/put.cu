@@ -322,7 +322,13 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   __shared__ uint32_t s_g;
   __shared__ LeaderState L;
   __shared__ DestDesc s_dests[kMaxRouterDests];   // destination descriptors, read every message
-  for (uint32_t d = lane; d < a.n_dests && d < (uint32_t)kMaxRouterDests; d += 32) s_dests[d] = a.dests[d];
+  if (a.n_dests == 1) {
+    if (lane == 0) s_dests[0] = a.dest0;
+  } else {
+    for (uint32_t d = lane; d < a.n_dests && d < (uint32_t)kMaxRouterDests; d += 32) s_dests[d] = a.dests[d];
+  }
+  // the fast path (one SPSC destination, no router) reads its state from the kernel parameters
+  const bool fast = !a.routes && a.n_dests == 1 && !a.dest0.mpsc;
   if (lane == 0) {
     L.loaded = 0;
     L.items = 0;
@@ -341,6 +347,11 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
       brief[lane].stage = mp->hdr.stage;
       brief[lane].nunits = units_for(len, a.chunk);
     }
+    uint64_t tc = 0, cq = 0;   // issued together with the brief loads (first round)
+    if (lane == 0 && fast && !(L.loaded & 1u)) {
+      tc = a.dest0.st->tail_cache;
+      cq = a.dest0.st->chan_seq;
+    }
     __syncwarp();
     if (lane == 0) {
       // Flow control: the round adds at most 2 items per message.
@@ -353,18 +364,18 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
       const uint32_t rnd = k0 / kGroup;
       if (a.trace && rnd < 64) a.trace[rnd * 4] = globaltimer();
       // the fast path needs destination 0's state and a fresh credit
-      if (!a.routes && !s_dests[0].mpsc) {
+      if (fast) {
         if (!(L.loaded & 1u)) {
           L.loaded |= 1u;
-          L.tails[0] = s_dests[0].st->tail_cache;
-          L.chans[0] = s_dests[0].st->chan_seq;
+          L.tails[0] = tc;
+          L.chans[0] = cq;
         }
-        L.heads[0] = read_head(s_dests[0]);
+        L.heads[0] = read_head(a.dest0);
       }
     }
     __syncwarp();
     uint32_t g = 0;
-    if (!a.routes && !s_dests[0].mpsc && !L.aborted) g = fast_place(a, ctx, L, gmax, gs, brief, s_dests[0]);
+    if (fast && !L.aborted) g = fast_place(a, ctx, L, gmax, gs, brief, a.dest0);
     if (g == 0) {
       if (lane == 0) s_g = leader_place(a, ctx, S, L, k0, gmax, gs, brief, s_dests);
       __syncwarp();

@@ -29,7 +29,10 @@ __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8
     int4* d = reinterpret_cast<int4*>(dst);
     const uint32_t n16 = (uint32_t)(nb >> 4);
     uint32_t i = lane;
-    constexpr int U = 16;   // 8 KiB in flight per warp
+#ifndef B200RING_COPY_U
+#define B200RING_COPY_U 16
+#endif
+    constexpr int U = B200RING_COPY_U;   // 16: 8 KiB in flight per warp
     for (; i + (U - 1) * 32 < n16; i += U * 32) {
       int4 v[U];
 #pragma unroll

@@ -118,6 +118,7 @@ struct Route {
 
 struct PutArgs {
   ring_msg_t inline_msg;  // used when msgs == nullptr (ring_put of one message)
+  DestDesc dest0;         // dests[0] by value (a peer's only destination: no load before placement)
   const ring_msg_t* msgs;
   uint32_t* status;
   uint32_t* dest_out;

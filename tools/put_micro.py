@@ -55,7 +55,7 @@ grids = [int(x) for x in (sys.argv[1:] or ["148", "296"])]
 MODES = [int(x) for x in os.environ.get("COPY_MODES", "0,1").split(",")]
 for ctas in grids:
   for mode in MODES:
-    for threads in (512,):
+    for threads in [int(x) for x in os.environ.get("THREADS", "256").split(",")]:
         R.ring_peer_config(peer, ctas, threads, mode)
         print(f"copy_mode={mode}")
         for name, m, plen in cases:
