@@ -124,19 +124,30 @@ HDR_BYTES = 64
 CRC_END = 56          # CRC covers header bytes [4, 56); [56, 64) is t_put (R10)
 
 
+HDR_FLAG_PAYLOAD_CRC = 1   # flags bit 0: bytes [40, 44) hold crc32(payload) (fault path, Q10)
+
+
 def encode_header(uid: bytes, accepted_at: int, app_id: int, stage: int, payload_len: int,
-                  producer_id: int, seq: int, epoch: int = 0, flags: int = 0, t_put: int = 0) -> bytes:
+                  producer_id: int, seq: int, epoch: int = 0, flags: int = 0, t_put: int = 0,
+                  payload_crc: int | None = None) -> bytes:
     """64-byte entry header.  Fields 4..44 follow the paper's message header
     (UUID, proxy timestamp, application ID, stage) in SPEC.md's
     order (uid16 accepted_at8 app_id4 stage2 payload_len4
     reserved6); bytes 44..56 are build extensions (producer id, channel seq,
     route epoch, flags) that make "message context / origin" visible
     (PAPER.md:630-631); bytes 56..64 hold a timing stamp outside the checksum.
-    Checksum: PAPER.md:768 "a checksum is applied to the data header"."""
+    Checksum: PAPER.md:768 "a checksum is applied to the data header".  With
+    `payload_crc` (the fault path's hardening: a header-only
+    checksum accepts torn payloads) bytes [40, 44) carry crc32(payload) and
+    flags bit 0 is set; both lie inside the header checksum."""
     assert len(uid) == 16
+    reserved = bytes(6)
+    if payload_crc is not None:
+        reserved = bytes(2) + struct.pack("<I", payload_crc)
+        flags |= HDR_FLAG_PAYLOAD_CRC
     body = (bytes(uid)
             + struct.pack("<QIHI", accepted_at, app_id, stage, payload_len)
-            + bytes(6)
+            + reserved
             + struct.pack("<IIHH", producer_id, seq, epoch, flags))
     assert len(body) == CRC_END - 4
     return struct.pack("<I", crc32(body)) + body + struct.pack("<Q", t_put)
@@ -148,9 +159,11 @@ def decode_header(h: bytes) -> dict:
     accepted_at, app_id, stage, payload_len = struct.unpack_from("<QIHI", h, 20)
     producer_id, seq, epoch, flags = struct.unpack_from("<IIHH", h, 44)
     t_put, = struct.unpack_from("<Q", h, 56)
+    payload_crc, = struct.unpack_from("<I", h, 40)
     return dict(crc=crc, uid=uid, accepted_at=accepted_at, app_id=app_id, stage=stage,
                 payload_len=payload_len, producer_id=producer_id, seq=seq, epoch=epoch,
-                flags=flags, t_put=t_put, crc_ok=(crc32(bytes(h[4:CRC_END])) == crc))
+                flags=flags, t_put=t_put, crc_ok=(crc32(bytes(h[4:CRC_END])) == crc),
+                payload_crc=payload_crc if flags & HDR_FLAG_PAYLOAD_CRC else None)
 
 
 # ----------------------------------------------------------------------------
