@@ -46,7 +46,10 @@ typedef enum {
   RING_ECORRUPT = 7,   /* header checksum mismatch: entry discarded and consumed */
   RING_ECUDA = 8,      /* a CUDA runtime call failed (see ring_last_cuda_error) */
   RING_EPEER = 9,      /* no peer access between the two devices / IPC open failed */
-  RING_EPENDING = 10   /* initial value of a device status word not yet written */
+  RING_EPENDING = 10,  /* initial value of a device status word not yet written */
+  RING_EDROPPED = 11   /* fault-tolerant ring: WL found the size slot taken -- the lock was taken over
+                          while this sender was delayed ("WL(X) fails due to the busy bit",
+                          PAPER.md:797); the message is dropped, no retransmission */
 } ring_status_t;
 
 /* flags for ring_put* / ring_get* */
@@ -57,6 +60,19 @@ typedef enum {
 /* flags for ring_create */
 #define RING_CREATE_DEFAULT 0u
 #define RING_CREATE_LOCAL 1u /* every producer runs on the ring's own device: gpu-scope ordering (cheaper fences) */
+/* The paper's liveness machinery, for senders that may be
+ * lost or delayed: the lock word is {acquisition count:48, owner+1:16}; a sender
+ * spinning on the lock takes it over (CAS old -> self) once it has observed
+ * the same word for the lock timeout (TL; local
+ * observation, no cross-GPU clock); GH publishes a committed entry a lost
+ * sender left behind (Case 7) or clears a stale write (R21); WL = CAS(slot,
+ * 0 -> busy|seq tag|f) (fails -> RING_EDROPPED); UH = CAS(tail, value read at
+ * GH -> new) (a taken-over sender cannot move the tail back, Q22); Unlock =
+ * CAS(self -> 0); every entry carries a payload CRC-32 in header bytes
+ * [40,44) (flags bit 0), checked by the consumer (torn payloads, Q10).
+ * Slot words gain a 22-bit sequence tag in bits 40-61 (R21).  Each message is
+ * appended with the sender's steps one at a time (no batching of publishes). */
+#define RING_CREATE_FAULT_TOLERANT 2u
 
 /* Geometry limits (R5, R8) */
 #define RING_ENTRY_ALIGN 128u
@@ -170,6 +186,29 @@ ring_status_t ring_put(ring_peer_t peer, const void* d_payload, uint64_t len, co
 ring_status_t ring_peer_config(ring_peer_t peer, uint32_t copy_ctas, uint32_t threads, uint32_t copy_mode);
 /* Host-side count of messages this attachment has submitted (= next header seq). */
 uint64_t ring_peer_submitted(ring_peer_t peer);
+
+/* ---- fault injection (tests of the fault-tolerant path) --------
+ * The labelled sender actions of PAPER.md:778-789 at which a put can be made to
+ * stop for good (a lost sender) or to pause (a delayed sender) while another
+ * sender takes the lock over.  Applies to message `msg` of every later launch
+ * of this attachment on a RING_CREATE_FAULT_TOLERANT ring. */
+#define RING_AT_LOCK 1u  /* after Lock (step 1) */
+#define RING_AT_GH 2u    /* after GH (steps 2-4: tail, head, stale-slot check) */
+#define RING_AT_WB 3u    /* after WB (step 5: header + payload written) */
+#define RING_AT_WL 4u    /* after WL (step 6) */
+#define RING_AT_UH 5u    /* after UH (step 7) */
+typedef struct {
+  uint32_t die_after;   /* RING_AT_*: stop right after this action (0 = never) */
+  uint32_t pause_mask;  /* bit (1 << RING_AT_*): after that action set arrived[l] = 1, then wait for go[l] != 0 */
+  uint32_t msg;         /* index of the message in the launch */
+  uint32_t reserved;
+  uint32_t* arrived;    /* pinned host memory (mapped), >= 8 words, written by the kernel */
+  uint32_t* go;         /* pinned host memory (mapped), >= 8 words, written by the host */
+} ring_fault_t;
+/* NULL clears.  RING_EINVAL unless the ring is fault tolerant. */
+ring_status_t ring_peer_set_fault(ring_peer_t peer, const ring_fault_t* fault);
+/* Lock timeout TL of fault-tolerant rings (default 200 us). */
+ring_status_t ring_set_lock_timeout_ns(uint64_t ns);
 
 /* ---- consumer ------------------------------------------------------------------
  * ring_get: receive the next `n` entries (receiver steps 1-3, PAPER.md:711-715,

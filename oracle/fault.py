@@ -517,11 +517,13 @@ def _act_for(sim: FaultSim, label: str):
     return ("step", pid)
 
 
-def replay_case(n: int, L: Layout, x_len: int, y_len: int, **kw) -> FaultSim:
-    """Run case n with one message per sender (lengths x_len, y_len), then let
-    the receiver drain.  Returns the simulator (inspect `.got`, `.log`)."""
-    progs = {0: [Msg(x_len, bytes([0xA0 + i % 16 for i in range(x_len)]))],
-             1: [Msg(y_len, bytes([0xB0 + i % 16 for i in range(y_len)]))]}
+def replay_case(n: int, L: Layout, x_len: int, y_len: int, progs: dict | None = None, **kw) -> FaultSim:
+    """Run case n with one message per sender (lengths x_len, y_len, or the
+    given one-message programs), then let the receiver drain.  Returns the
+    simulator (inspect `.got`, `.log`)."""
+    if progs is None:
+        progs = {0: [Msg(x_len, bytes([0xA0 + i % 16 for i in range(x_len)]))],
+                 1: [Msg(y_len, bytes([0xB0 + i % 16 for i in range(y_len)]))]}
     sim = FaultSim(L, progs, max_crashes=1, max_live_steals=1, **kw)
     for lab in CASES[n]:
         a = _act_for(sim, lab)

@@ -84,7 +84,8 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
     // ---- slots of every published entry (one per lane)
     uint64_t w = 0;
     if ((uint32_t)lane < e) w = ld_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(G) + lane));
-    const uint64_t f = (uint32_t)lane < e ? (w & kFMask) : 0;
+    // footprint: bits 0-39 (fault-tolerant rings keep a sequence tag in 40-61, R21; R < 2^40)
+    const uint64_t f = (uint32_t)lane < e ? (w & ((1ull << 40) - 1)) : 0;
     const bool pad = (w & kPad) != 0;
     const bool ismsg = (uint32_t)lane < e && !pad;
     const uint64_t incl = warp_incl_scan64(f, lane);
@@ -106,9 +107,9 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
     uint64_t len = 0;
     uint32_t status = RING_OK;
     bool deliver = false;
+    uint32_t hw[16] = {};
     if (in && ismsg) {
       const int4* hp = reinterpret_cast<const int4*>(a.data + start);
-      uint32_t hw[16];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int4 v = __ldcg(hp + q);
@@ -119,6 +120,18 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
       if (crc != hw[0] || kHdr + len > f) { status = RING_ECORRUPT; len = 0; }   // discarded, still consumed
       else if (copy && len > a.dst_stride) status = RING_EMSGSIZE;
       else deliver = true;
+    }
+    // payload checksum (header flags bit 0, fault-tolerant rings, Q10): one warp per entry
+    uint32_t pmask = __ballot_sync(0xffffffffu, in && ismsg && status != RING_ECORRUPT && ((hw[13] >> 16) & 1u));
+    while (pmask) {
+      const int j = __ffs(pmask) - 1;
+      pmask &= pmask - 1;
+      const uint64_t sj = __shfl_sync(0xffffffffu, start, j);
+      const uint64_t lj = __shfl_sync(0xffffffffu, len, j);
+      const uint32_t c = warp_crc32(a.data + sj + kHdr, lj, crc_tab, a.crc_table + kCrcTableWords, lane);
+      if (lane == j && c != hw[10]) { status = RING_ECORRUPT; len = 0; deliver = false; }
+    }
+    if (in && ismsg) {
       ring_view_t* v = a.views + mi;
       v->offset = start + kHdr;
       v->len = len;

@@ -23,6 +23,7 @@ namespace {
 
 thread_local char g_cuda_err[512] = "";
 std::atomic<uint64_t> g_timeout_ns{2000000000ull};
+std::atomic<uint64_t> g_lock_timeout_ns{200000ull};   // TL of fault-tolerant rings
 std::atomic<uint64_t> g_launches{0};
 std::mutex g_mu;
 const uint32_t g_token = 0x9e3779b9u ^ (uint32_t)getpid() ^ (uint32_t)((uintptr_t)&g_mu & 0xffffffffu);
@@ -72,8 +73,25 @@ struct DevGuard {
 // Table 0 is the standard 256-entry table of the reflected CRC-32
 // (0xEDB88320), built from this file's own shift-register step; table k
 // advances table k-1 by one more zero byte.  Kernels consume 4 bytes per step.
+// Slicing-by-4 tables (kCrcTableWords), then kCrcPowWords powers
+// x^(2^n) mod P (reflected) for combining CRCs of adjacent byte ranges.
+static uint32_t gf2_mulmod(uint32_t a, uint32_t b) {
+  uint32_t m = 1u << 31, p = 0;
+  for (;;) {
+    if (a & m) {
+      p ^= b;
+      if ((a & (m - 1)) == 0) break;
+    }
+    m >>= 1;
+    b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+  }
+  return p;
+}
 std::vector<uint32_t> build_crc_table() {
-  std::vector<uint32_t> t(kCrcTableWords);
+  std::vector<uint32_t> t(kCrcTableWords + kCrcPowWords);
+  uint32_t* pw = t.data() + kCrcTableWords;
+  pw[0] = 1u << 30;   // x^1
+  for (int n = 1; n < kCrcPowWords; ++n) pw[n] = gf2_mulmod(pw[n - 1], pw[n - 1]);
   for (uint32_t i = 0; i < 256; ++i) {
     uint32_t reg = i;
     for (int b = 0; b < 8; ++b) reg = (reg & 1) ? (reg >> 1) ^ 0xEDB88320u : reg >> 1;
@@ -154,6 +172,7 @@ struct ring_peer_s {
   uint32_t copy_ctas = 0, threads = 0, chunk = 0, copy_mode = 0;
   uint64_t* trace = nullptr;                 // debug timeline (B200RING_TRACE=1)
   const uint32_t* crc = nullptr;
+  FaultSpec fault;                           // test-only fault injection (fault-tolerant rings)
 };
 
 struct router_s {
@@ -185,10 +204,16 @@ const char* ring_strerror(ring_status_t s) {
     case RING_ECUDA: return "CUDA error";
     case RING_EPEER: return "no peer access / IPC failure";
     case RING_EPENDING: return "pending";
+    case RING_EDROPPED: return "dropped: size slot taken after a lock take-over";
   }
   return "unknown";
 }
 const char* ring_last_cuda_error(void) { return g_cuda_err; }
+ring_status_t ring_set_lock_timeout_ns(uint64_t ns) {
+  if (ns == 0) return RING_EINVAL;
+  g_lock_timeout_ns = ns;
+  return RING_OK;
+}
 ring_status_t ring_set_timeout_ns(uint64_t ns) {
   if (ns == 0) return RING_EINVAL;
   g_timeout_ns = ns;
@@ -361,7 +386,8 @@ ring_status_t ring_attach_peer(const ring_handle_t* h, int producer_device, uint
   p->desc.st = p->st;
   p->desc.R = b.R;
   p->desc.N = b.N;
-  p->desc.mpsc = b.max_producers > 1 ? 1u : 0u;
+  p->desc.ft = (b.flags & RING_CREATE_FAULT_TOLERANT) ? 1u : 0u;
+  p->desc.mpsc = (b.max_producers > 1 || p->desc.ft) ? 1u : 0u;   // fault tolerance needs the lock
   p->desc.producer_id = producer_id;
   p->desc.has_mirror = 0;
   p->desc.sys = (same_process && producer_device == b.device) ? 0u : 1u;
@@ -443,6 +469,22 @@ ring_status_t ring_peer_config(ring_peer_t p, uint32_t copy_ctas, uint32_t threa
 
 uint64_t ring_peer_submitted(ring_peer_t p) { return p ? p->base : 0; }
 
+ring_status_t ring_peer_set_fault(ring_peer_t p, const ring_fault_t* f) {
+  if (!p || !p->desc.ft) return RING_EINVAL;
+  if (!f) {
+    p->fault = FaultSpec{};
+    return RING_OK;
+  }
+  if (f->die_after > RING_AT_UH || (f->pause_mask & ~0x3Eu) || (f->pause_mask && (!f->arrived || !f->go)))
+    return RING_EINVAL;
+  p->fault.die_after = f->die_after;
+  p->fault.pause_mask = f->pause_mask;
+  p->fault.msg = f->msg;
+  p->fault.arrived = f->arrived;
+  p->fault.go = f->go;
+  return RING_OK;
+}
+
 ring_status_t ring_peer_trace(ring_peer_t p, uint64_t* host_out, uint32_t n) {
   if (!p || !host_out) return RING_EINVAL;
   if (!p->trace) return RING_EINVAL;
@@ -492,6 +534,8 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   a.dests = p->desc_dev;
   a.dest0 = p->desc;
   a.n_dests = 1;
+  a.lock_timeout_ns = g_lock_timeout_ns;
+  a.fault = p->fault;
   a.crc_table = p->crc;
   a.timeout_ns = g_timeout_ns;
   a.n = n;

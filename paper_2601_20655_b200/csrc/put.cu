@@ -315,6 +315,215 @@ __device__ uint32_t fast_place(const PutArgs& a, LaunchCtx* ctx, LeaderState& L,
   return run;
 }
 
+// ---------------------------------------------------------------------------
+// Fault-tolerant sender (RING_CREATE_FAULT_TOLERANT, the
+// oracle's FaultSim step for step).  One message at a time, every action by
+// lane 0 of the leader warp except WB's payload, which the copy warps move
+// (one plan item per message; the publisher only counts it).  Tagged slot
+// words: busy | pad | (seq mod 2^22) << 40 | f (reading R21).
+// ---------------------------------------------------------------------------
+constexpr int kTagShift = 40;
+constexpr uint64_t kTagMask = (1ull << 22) - 1;
+constexpr uint64_t kFLow = (1ull << kTagShift) - 1;
+__device__ __forceinline__ uint64_t tagged_word(uint64_t w, uint32_t q) { return w | ((q & kTagMask) << kTagShift); }
+
+template <bool SYS>
+__device__ __forceinline__ uint64_t dcas(uint64_t* p, uint64_t cmp, uint64_t val) { return cas_acq_rel<SYS>(p, cmp, val); }
+__device__ __forceinline__ uint64_t dcas(const DestDesc& D, uint64_t* p, uint64_t cmp, uint64_t val) {
+  return D.sys ? dcas<true>(p, cmp, val) : dcas<false>(p, cmp, val);
+}
+__device__ __forceinline__ uint64_t dld(const DestDesc& D, const uint64_t* p) {
+  return D.sys ? ld_acquire<true>(p) : ld_acquire<false>(p);
+}
+
+// Fault injection point `at` for message k (lane 0).  Returns true if the
+// sender must stop for good here.
+__device__ bool ft_point(const PutArgs& a, uint32_t at, uint32_t k, uint64_t timeout_ns) {
+  const FaultSpec& F = a.fault;
+  if (k != F.msg) return false;
+  if (F.pause_mask & (1u << at)) {
+    volatile uint32_t* arr = F.arrived;
+    volatile uint32_t* go = F.go;
+    __threadfence_system();
+    arr[at] = 1u;
+    __threadfence_system();
+    const uint64_t t0 = globaltimer();
+    while (go[at] == 0u)
+      if (globaltimer() - t0 > timeout_ns) break;
+    __threadfence_system();
+  }
+  return F.die_after == at;
+}
+
+__device__ void ft_put(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, uint32_t* s_crc) {
+  const int lane = threadIdx.x & 31;
+  const DestDesc& D = a.dest0;
+  for (int i = lane; i < kCrcTableWords; i += 32) s_crc[i] = a.crc_table[i];
+  __syncwarp();
+  const uint32_t* pw = a.crc_table + kCrcTableWords;
+  uint64_t chan = 0, acq = 0;
+  if (lane == 0) { chan = D.st->chan_seq; acq = D.st->lock_acq; }
+  chan = __shfl_sync(0xffffffffu, chan, 0);
+  uint32_t items = 0, units = 0;
+  bool dead = false;
+  const uint64_t t_begin = globaltimer();
+  for (uint32_t k = 0; k < a.n && !dead; ++k) {
+    const ring_msg_t* mp = a.msgs ? a.msgs + k : &a.inline_msg;
+    const uint64_t len = mp->len;
+    const uint64_t f = footprint(len);
+    uint32_t status = RING_OK;
+    if (len >= (1ull << 32) || f > D.R) status = RING_EMSGSIZE;
+    // payload checksum first: it goes into the header (bytes [40,44))
+    const uint32_t pcrc = status == RING_OK ? warp_crc32(reinterpret_cast<const uint8_t*>(mp->src), len, s_crc, pw, lane) : 0u;
+    uint64_t P = 0, me = 0;
+    uint32_t st = status, die = 0;
+    if (lane == 0 && st == RING_OK) {
+      const uint64_t t_msg = globaltimer();
+      bool have_lock = false;
+      uint64_t seen = 0, seen_at = 0;
+      while (st == RING_OK) {                                   // ---- step 1: Lock (+ TL take-over)
+        if (!have_lock) {
+          me = (++acq << 16) | (uint64_t)(D.producer_id + 1);
+          while (true) {
+            const uint64_t old = dcas(D, lock_w(D), 0ull, me);
+            if (old == 0) break;
+            const uint64_t now = globaltimer();
+            if (old != seen) { seen = old; seen_at = now; }
+            else if (now - seen_at > a.lock_timeout_ns) {     // TL: the holder is presumed lost
+              if (dcas(D, lock_w(D), old, me) == old) break;
+            }
+            if (now - t_msg > a.timeout_ns) { st = RING_ETIMEDOUT; break; }
+          }
+          if (st != RING_OK) break;
+          have_lock = true;
+          if (ft_point(a, RING_AT_LOCK, k, a.timeout_ns)) { die = 1; break; }
+        }
+        // ---- steps 2-4: GH (tail, head, next slot: repair a lost sender's entry / clear a stale write)
+        P = dld(D, tail_w(D));
+        const uint64_t H = read_head(D);
+        const uint32_t pq = ptr_seq(P), hq = ptr_seq(H);
+        const uint64_t pb = ptr_off(P), hb = ptr_off(H);
+        if (seq_dist(pq, hq) < D.N) {
+          const uint64_t w = dld(D, slot_w(D, pq));
+          if (w & kBusy) {
+            if (((w >> kTagShift) & kTagMask) == (pq & kTagMask))      // Case 7: publish it
+              dcas(D, tail_w(D), P, pack_ptr(advance(pb, w & kFLow, D.R), seq_inc(pq)));
+            else                                                        // R21: stale write
+              dcas(D, slot_w(D, pq), w, 0ull);
+            continue;
+          }
+        }
+        // ---- step 3: space (R4), PAD at the wrap (R3)
+        bool full = seq_dist(pq, hq) >= D.N;
+        if (!full && pb + f > D.R) {
+          if (span_free(pb, pq, hb, hq, D.R - pb)) {
+            if (dcas(D, slot_w(D, pq), 0ull, tagged_word(kBusy | kPad | (D.R - pb), pq)) == 0ull)
+              dcas(D, tail_w(D), P, pack_ptr(0, seq_inc(pq)));
+            continue;                                           // re-read (GH) after the PAD
+          }
+          full = true;
+        } else if (!full && !span_free(pb, pq, hb, hq, f)) {
+          full = true;
+        }
+        if (full) {                                             // unlock, wait for the head, start over
+          if (a.flags & RING_TRY) { dcas(D, lock_w(D), me, 0ull); st = RING_FULL; break; }
+          dcas(D, lock_w(D), me, 0ull);
+          have_lock = false;
+          while (read_head(D) == H)
+            if (globaltimer() - t_msg > a.timeout_ns) { st = RING_ETIMEDOUT; break; }
+          continue;
+        }
+        if (ft_point(a, RING_AT_GH, k, a.timeout_ns)) { die = 1; break; }
+        break;                                                  // placement decided: P
+      }
+      if (st != RING_OK && !die) {
+        // nothing written (FULL / timeout); the lock is ours only if still held
+        if (me) dcas(D, lock_w(D), me, 0ull);
+      }
+    }
+    st = __shfl_sync(0xffffffffu, st, 0);
+    die = __shfl_sync(0xffffffffu, die, 0);
+    P = __shfl_sync(0xffffffffu, P, 0);
+    me = __shfl_sync(0xffffffffu, me, 0);
+    if (die) { dead = true; break; }
+    if (st == RING_OK) {
+      // ---- step 5: WB -- header (lanes 0-3) and payload (copy warps)
+      const uint64_t start = ptr_off(P);
+      if (lane < 4) {
+        uint32_t w[16];
+        const uint32_t* uid = reinterpret_cast<const uint32_t*>(mp->hdr.uid);
+        const uint32_t len32 = (uint32_t)len;
+        w[1] = uid[0]; w[2] = uid[1]; w[3] = uid[2]; w[4] = uid[3];
+        w[5] = (uint32_t)mp->hdr.accepted_at;
+        w[6] = (uint32_t)(mp->hdr.accepted_at >> 32);
+        w[7] = mp->hdr.app_id;
+        w[8] = (uint32_t)mp->hdr.stage | (len32 << 16);
+        w[9] = len32 >> 16;
+        w[10] = pcrc;                                  // reserved[40,44): payload CRC
+        w[11] = D.producer_id;
+        w[12] = (uint32_t)(chan + k);
+        w[13] = 1u << 16;                              // epoch 0, flags bit 0: payload CRC present
+        w[0] = crc52(w, s_crc);
+        const uint64_t t = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();
+        w[14] = (uint32_t)t;
+        w[15] = (uint32_t)(t >> 32);
+        st16(D.data + start + 16 * lane, make_int4((int)w[4 * lane], (int)w[4 * lane + 1], (int)w[4 * lane + 2],
+                                                   (int)w[4 * lane + 3]));
+      }
+      const uint32_t nu = units_for(len, a.chunk);
+      if (lane == 0) {
+        Plan& p = ctx->plan[items % kPlanRing];
+        p.src = mp->src;
+        p.dst = reinterpret_cast<uint64_t>(D.data + start + kHdr);
+        p.len = len;
+        p.first_unit = units;
+        p.nunits = nu;
+        p.flags = 0;                                   // the publisher only counts it
+        p.msg = k;
+        S->arrive[items % kPlanRing] = 0;
+        st_release<false>(&S->planned, make_planned(items + 1, units + nu));
+        const uint64_t t0 = globaltimer();
+        while (nu && ld_acquire_gpu32(&S->arrive[items % kPlanRing]) != nu)
+          if (globaltimer() - t0 > a.timeout_ns) break;
+      }
+      ++items;
+      units += nu;
+      __syncwarp();
+      if (lane == 0) {
+        if (ft_point(a, RING_AT_WB, k, a.timeout_ns)) die = 1;
+        // ---- step 6: WL = CAS(slot, 0 -> busy|tag|f); release: WB before WL (a GH repair may publish it)
+        if (!die) {
+          const uint32_t pq = ptr_seq(P);
+          if (dcas(D, slot_w(D, pq), 0ull, tagged_word(kBusy | f, pq)) != 0ull) {
+            st = RING_EDROPPED;
+            dcas(D, lock_w(D), me, 0ull);                          // Unlock (may fail: taken over)
+          } else {
+            if (ft_point(a, RING_AT_WL, k, a.timeout_ns)) die = 1;
+            // ---- step 7: UH = CAS(tail, P -> new); failing = committed, a later GH publishes it
+            if (!die) {
+              dcas(D, tail_w(D), P, pack_ptr(advance(ptr_off(P), f, D.R), seq_inc(pq)));
+              if (ft_point(a, RING_AT_UH, k, a.timeout_ns)) die = 1;
+            }
+            if (!die) dcas(D, lock_w(D), me, 0ull);                // ---- step 8: Unlock = CAS(me -> 0)
+          }
+        }
+      }
+      st = __shfl_sync(0xffffffffu, st, 0);
+      die = __shfl_sync(0xffffffffu, die, 0);
+      if (die) { dead = true; break; }
+    }
+    if (lane == 0) a.status[k] = st;
+  }
+  (void)t_begin;
+  if (lane == 0) {
+    st_release<false>(&S->planned, make_planned(items, units) | kPlannedDone);
+    if (!dead) {
+      D.st->chan_seq = chan + a.n;
+      D.st->lock_acq = acq;
+    }
+  }
+}
+
 __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   const int lane = threadIdx.x & 31;
   __shared__ GroupSlot gs[kGroup];
@@ -615,7 +824,8 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
     if (a.trace && threadIdx.x == 0) a.trace[252] = globaltimer();
     if (warp == 0) {
       reset_set(&ctx->set[(a.launch + 1) & 1], lane);
-      put_leader(a, ctx, S);
+      if (a.dest0.ft && !a.routes) ft_put(a, ctx, S, s_crc);
+      else put_leader(a, ctx, S);
       return;
     }
     if (warp == 1) {   // the publisher writes the headers: it holds the CRC tables

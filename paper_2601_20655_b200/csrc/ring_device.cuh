@@ -93,6 +93,13 @@ __device__ __forceinline__ uint64_t cas_acquire(uint64_t* p, uint64_t cmp, uint6
   else asm volatile("atom.acquire.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(val) : "memory");
   return old;
 }
+template <bool SYS>
+__device__ __forceinline__ uint64_t cas_acq_rel(uint64_t* p, uint64_t cmp, uint64_t val) {
+  uint64_t old;
+  if (SYS) asm volatile("atom.acq_rel.sys.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(val) : "memory");
+  else asm volatile("atom.acq_rel.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(val) : "memory");
+  return old;
+}
 // Launch-local coordination (all on the producer's own GPU): gpu scope.
 __device__ __forceinline__ uint64_t ld_acquire_gpu64(const uint64_t* p) { return ld_acquire<false>(p); }
 __device__ __forceinline__ uint32_t ld_acquire_gpu32(const uint32_t* p) {
@@ -162,6 +169,7 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu32(const uint32_t* p) {
 // once.
 // ---------------------------------------------------------------------------
 constexpr int kCrcTableWords = 4 * 256;
+constexpr int kCrcPowWords = 32;   // after the tables in the global copy: x^(2^n) mod P
 __device__ __forceinline__ uint32_t crc52(const uint32_t* w, const uint32_t* __restrict__ tab) {
   uint32_t c = 0xFFFFFFFFu;
 #pragma unroll
@@ -170,6 +178,64 @@ __device__ __forceinline__ uint32_t crc52(const uint32_t* w, const uint32_t* __r
     c = tab[3 * 256 + (c & 0xFFu)] ^ tab[2 * 256 + ((c >> 8) & 0xFFu)] ^ tab[256 + ((c >> 16) & 0xFFu)] ^ tab[c >> 24];
   }
   return ~c;
+}
+
+// ---------------------------------------------------------------------------
+// CRC-32/IEEE of a byte range (the fault-tolerant rings' payload checksum,
+// SURVEY.md Q10), one warp per range: lane l takes a contiguous slice, the
+// slice CRCs are combined with crc(A || B) = (crc(A) * x^(8|B|) mod P) ^ crc(B)
+// (GF(2) multiply by a power of x built from the x^(2^n) table `pw`).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t gf2_mulmod_dev(uint32_t a, uint32_t b) {
+  uint32_t p = 0;
+  for (int i = 31; i >= 0; --i) {
+    if (a & (1u << i)) p ^= b;
+    b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+  }
+  return p;
+}
+// x^(8 n) mod P
+__device__ __forceinline__ uint32_t x8n_mod(uint64_t n, const uint32_t* __restrict__ pw) {
+  uint32_t p = 1u << 31;   // x^0
+  int k = 3;
+  while (n) {
+    if (n & 1) p = gf2_mulmod_dev(pw[k & 31], p);
+    n >>= 1;
+    ++k;
+  }
+  return p;
+}
+__device__ __forceinline__ uint32_t crc32_combine_dev(uint32_t c1, uint32_t c2, uint64_t len2, const uint32_t* pw) {
+  return len2 ? gf2_mulmod_dev(x8n_mod(len2, pw), c1) ^ c2 : c1;
+}
+__device__ __forceinline__ uint32_t crc32_range(const uint8_t* p, uint64_t n, const uint32_t* __restrict__ tab) {
+  uint32_t c = 0xFFFFFFFFu;
+  uint64_t i = 0;
+  for (; i < n && ((uintptr_t)(p + i) & 3); ++i) c = tab[(c ^ __ldcg(p + i)) & 0xFFu] ^ (c >> 8);
+  for (; i + 4 <= n; i += 4) {
+    c ^= __ldcg(reinterpret_cast<const uint32_t*>(p + i));
+    c = tab[3 * 256 + (c & 0xFFu)] ^ tab[2 * 256 + ((c >> 8) & 0xFFu)] ^ tab[256 + ((c >> 16) & 0xFFu)] ^ tab[c >> 24];
+  }
+  for (; i < n; ++i) c = tab[(c ^ __ldcg(p + i)) & 0xFFu] ^ (c >> 8);
+  return ~c;
+}
+// Whole-warp CRC of [p, p + n); every lane returns the result.
+__device__ __forceinline__ uint32_t warp_crc32(const uint8_t* p, uint64_t n, const uint32_t* tab, const uint32_t* pw,
+                                               int lane) {
+  const uint64_t slice = ((n + 31) / 32 + 15) & ~15ull;
+  const uint64_t lo = min(n, (uint64_t)lane * slice), hi = min(n, lo + slice);
+  uint32_t c = crc32_range(p + lo, hi - lo, tab);
+  uint64_t len = hi - lo;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {     // tree: lane l (multiple of 2s) absorbs lane l + s
+    const uint32_t c2 = __shfl_down_sync(0xffffffffu, c, s);
+    const uint64_t l2 = __shfl_down_sync(0xffffffffu, len, s);
+    if ((lane & (2 * s - 1)) == 0) {
+      c = crc32_combine_dev(c, c2, l2, pw);
+      len += l2;
+    }
+  }
+  return __shfl_sync(0xffffffffu, c, 0);
 }
 
 }  // namespace b200ring

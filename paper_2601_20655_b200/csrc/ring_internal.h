@@ -22,7 +22,8 @@ struct alignas(128) DestState {
   uint64_t _p0[15];
   uint64_t tail_cache;   // SPSC: tail after the last planned entry (leader-owned)
   uint64_t chan_seq;     // next header seq of this channel (R18)
-  uint64_t _p1[14];
+  uint64_t lock_acq;     // fault-tolerant rings: lock acquisitions by this attachment
+  uint64_t _p1[13];
 };
 static_assert(sizeof(DestState) == 256, "DestState layout");
 
@@ -37,7 +38,17 @@ struct DestDesc {
   uint32_t producer_id;
   uint32_t has_mirror;   // unused by the kernels (mirror validity is in-band)
   uint32_t sys;          // 1: ring / consumer on another GPU -> .sys scope
-  uint32_t _pad;
+  uint32_t ft;           // RING_CREATE_FAULT_TOLERANT: take-over, CAS WL/UH/Unlock, tags, payload CRC
+};
+
+// Test-only fault injection of a put launch (ring_peer_set_fault).
+struct FaultSpec {
+  uint32_t die_after = 0;
+  uint32_t pause_mask = 0;
+  uint32_t msg = 0;
+  uint32_t _r = 0;
+  uint32_t* arrived = nullptr;
+  uint32_t* go = nullptr;
 };
 
 enum PlanFlags : uint32_t {
@@ -136,6 +147,8 @@ struct PutArgs {
   uint32_t chunk;             // bytes per copy work unit
   uint32_t copy_mode;         // 0: LSU copy warps, 1: TMA engine per CTA
   uint32_t _pad;
+  uint64_t lock_timeout_ns;   // TL (fault-tolerant rings)
+  FaultSpec fault;            // test-only fault injection
 };
 
 constexpr int kEngineStages = 4;   // TMA engine: shared-memory stages of `chunk` bytes

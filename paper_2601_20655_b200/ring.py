@@ -18,11 +18,12 @@ LIB_PATH = os.path.join(_HERE, "libb200ring.so")
 
 # ---- status codes / flags (include/b200ring.h) ------------------------------------
 RING_OK, RING_EINVAL, RING_ENOMEM, RING_EMSGSIZE, RING_FULL, RING_EMPTY = 0, 1, 2, 3, 4, 5
-RING_ETIMEDOUT, RING_ECORRUPT, RING_ECUDA, RING_EPEER, RING_EPENDING = 6, 7, 8, 9, 10
+RING_ETIMEDOUT, RING_ECORRUPT, RING_ECUDA, RING_EPEER, RING_EPENDING, RING_EDROPPED = 6, 7, 8, 9, 10, 11
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EMSGSIZE", 4: "FULL", 5: "EMPTY", 6: "ETIMEDOUT",
-                7: "ECORRUPT", 8: "ECUDA", 9: "EPEER", 10: "EPENDING"}
+                7: "ECORRUPT", 8: "ECUDA", 9: "EPEER", 10: "EPENDING", 11: "EDROPPED"}
 RING_BLOCK, RING_TRY, RING_NO_TIMESTAMP = 0, 1, 2
-RING_CREATE_DEFAULT, RING_CREATE_LOCAL = 0, 1
+RING_CREATE_DEFAULT, RING_CREATE_LOCAL, RING_CREATE_FAULT_TOLERANT = 0, 1, 2
+RING_AT_LOCK, RING_AT_GH, RING_AT_WB, RING_AT_WL, RING_AT_UH = 1, 2, 3, 4, 5
 RING_HDR_BYTES, RING_ENTRY_ALIGN = 64, 128
 
 
@@ -33,6 +34,11 @@ class ring_hdr_t(C.Structure):
 
 class ring_handle_t(C.Structure):
     _fields_ = [("bytes", C.c_ubyte * 128)]
+
+
+class ring_fault_t(C.Structure):
+    _fields_ = [("die_after", C.c_uint32), ("pause_mask", C.c_uint32), ("msg", C.c_uint32),
+                ("reserved", C.c_uint32), ("arrived", C.c_void_p), ("go", C.c_void_p)]
 
 
 class ring_info_t(C.Structure):
@@ -88,6 +94,8 @@ def _load():
         "ring_set_timeout_ns": [U64],
         "ring_clock_offset_ns": [I, C.POINTER(C.c_int64)],
         "ring_peer_trace": [P, P, U32],
+        "ring_peer_set_fault": [P, C.POINTER(ring_fault_t)],
+        "ring_set_lock_timeout_ns": [U64],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -302,3 +310,21 @@ def make_msgs(srcs, lens, uids, accepted_at, app_ids, stages) -> np.ndarray:
 def parse_views(raw: np.ndarray) -> np.ndarray:
     """Interpret a uint8 host array of n*128 bytes as ring_view_t records."""
     return np.ascontiguousarray(raw, dtype=np.uint8).view(VIEW_DTYPE)
+
+
+# ---- fault injection (tests of RING_CREATE_FAULT_TOLERANT rings) ---------------------
+def ring_peer_set_fault(peer: int, die_after: int = 0, pause_mask: int = 0, msg: int = 0,
+                        arrived=None, go=None) -> None:
+    """Make message `msg` of later launches stop for good after action `die_after`
+    (RING_AT_*) and/or pause after the actions in `pause_mask` until the host
+    sets go[l]; `arrived` / `go` are pinned host tensors (>= 8 int32 words).
+    All zeros clears."""
+    if not (die_after or pause_mask):
+        _check("ring_peer_set_fault", lib.ring_peer_set_fault(peer, None))
+        return
+    f = ring_fault_t(die_after, pause_mask, msg, 0, _ptr(arrived), _ptr(go))
+    _check("ring_peer_set_fault", lib.ring_peer_set_fault(peer, C.byref(f)))
+
+
+def ring_set_lock_timeout_ns(ns: int) -> None:
+    _check("ring_set_lock_timeout_ns", lib.ring_set_lock_timeout_ns(int(ns)))
