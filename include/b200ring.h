@@ -47,9 +47,10 @@ typedef enum {
   RING_ECUDA = 8,      /* a CUDA runtime call failed (see ring_last_cuda_error) */
   RING_EPEER = 9,      /* no peer access between the two devices / IPC open failed */
   RING_EPENDING = 10,  /* initial value of a device status word not yet written */
-  RING_EDROPPED = 11   /* fault-tolerant ring: WL found the size slot taken -- the lock was taken over
+  RING_EDROPPED = 11,  /* fault-tolerant ring: WL found the size slot taken -- the lock was taken over
                           while this sender was delayed ("WL(X) fails due to the busy bit",
                           PAPER.md:797); the message is dropped, no retransmission */
+  RING_EREJECTED = 12  /* routed put: refused by the route's admission control (fast reject) */
 } ring_status_t;
 
 /* flags for ring_put* / ring_get* */
@@ -187,6 +188,54 @@ ring_status_t ring_peer_config(ring_peer_t peer, uint32_t copy_ctas, uint32_t th
 /* Host-side count of messages this attachment has submitted (= next header seq). */
 uint64_t ring_peer_submitted(ring_peer_t peer);
 
+/* ---- lock-free fan-in ----------
+ * Instead of one MPSC ring whose producers serialise on the lock (PAPER.md:697,
+ * 706), give every producer its own single-producer ring (max_producers = 1,
+ * lock elided, R14) on the consumer GPU and serve them all with ONE consumer
+ * warp: lane i polls ring i's tail and runs the receiver steps 1-5 on it, all
+ * rings in parallel, one entry per ring per round, rounds starting at a
+ * rotating ring (no producer starves).  Per-channel order = each ring's FIFO;
+ * the merged order is the consumer's round order. */
+typedef struct ring_set_s* ring_set_t;
+/* 1 <= n <= 32 rings, all on one device; their producers must be bound
+ * (ring_bind_mirror) before consuming.  The rings must only be read through
+ * the set afterwards (its consume releases every entry it reads). */
+ring_status_t ring_set_create(const ring_t* rings, uint32_t n, ring_set_t* out);
+ring_status_t ring_set_destroy(ring_set_t set);
+/* Receive and release the next `n` messages from any ring of the set: view
+ * records as ring_consume (reserved[0] = ring index) and, if not NULL, the ring
+ * index of each in d_ring_idx (device, n words).  RING_TRY: stop at the first
+ * round with nothing to read (remaining views RING_EMPTY). */
+ring_status_t ring_set_consume(ring_set_t set, uint32_t n, ring_view_t* d_views, uint32_t* d_ring_idx, uint32_t flags,
+                               void* stream);
+
+/* ---- fused device-side put -------------------
+ * A producer kernel can write its output straight into the peer ring slot and
+ * publish it itself (include/b200ring_device.cuh: grid_reserve / payload_ptr /
+ * grid_commit), saving the output's HBM round trip and the put launch.  This
+ * is the device-side view of a single-producer attachment it needs.  The
+ * attachment must not be used by ring_put* concurrently. */
+typedef struct {
+  uint64_t ring;         /* ring base in the producer's address space */
+  uint64_t data;         /* buffer region */
+  uint64_t state;        /* producer-local state: head mirror, tail cache, channel counter */
+  uint64_t ctl;          /* 128-B grid-coordination block of this attachment */
+  uint64_t crc_table;    /* CRC-32 tables on the producer device */
+  uint64_t R;
+  uint32_t N;
+  uint32_t producer_id;
+  uint32_t sys;          /* 1: system-scope ordering (ring on another GPU) */
+  uint32_t reserved;
+} ring_dev_peer_t;
+/* RING_EINVAL for a multi-producer (locked) ring. */
+ring_status_t ring_peer_device_view(ring_peer_t peer, ring_dev_peer_t* out);
+/* A synthetic stage with a fused put epilogue: out = bf16(in * scale) for
+ * `n_elems` bf16 elements of `d_in`, written by the computing threads directly
+ * into the next entry of the peer ring (one message of 2 * n_elems bytes,
+ * header from `hdr`), in ONE launch.  Status word as ring_put. */
+ring_status_t ring_stage_scale_bf16_put(ring_peer_t peer, const void* d_in, uint64_t n_elems, float scale,
+                                        const ring_hdr_t* hdr, uint32_t flags, uint32_t* d_status, void* stream);
+
 /* ---- fault injection (tests of the fault-tolerant path) --------
  * The labelled sender actions of PAPER.md:778-789 at which a put can be made to
  * stop for good (a lost sender) or to pause (a delayed sender) while another
@@ -263,6 +312,25 @@ ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, cons
  * The chosen destination index is written to d_dest (device, n words) if not NULL. */
 ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, uint32_t flags, uint32_t* d_status,
                               uint32_t* d_dest, void* stream);
+/* Fast reject ("whenever the incoming request rate exceeds
+ * K/T_X, the proxy rejects additional requests"): routed puts to (app_id,
+ * stage) are admitted at rate k / t_x with burst 1, by arrival time =
+ * hdr.accepted_at (the proxy's timestamp), in the units
+ * t_x is given in: a message arriving at t is admitted iff t >= next, then
+ * next = max(next, t) + t_x / k (exact integer arithmetic on t * k).
+ * Rejected messages get RING_EREJECTED and are never sent.  k = 0 disables.
+ * The route must exist (router_set_route). */
+ring_status_t router_set_admission(router_t r, uint32_t app_id, uint16_t stage, uint64_t t_x, uint32_t k,
+                                   void* stream);
+/* Theorem 1: M = ceil(K * T_Y / T_X) instances of stage Y
+ * give it the output rate K / T_X of stage X.  0 on bad input (t_x or t_y 0, k 0). */
+uint64_t ring_required_instances(uint64_t t_x, uint64_t t_y, uint32_t k);
+/* Size a route by Theorem 1 and drive it: route (app_id, stage) to the first
+ * M = ring_required_instances(t_x, t_y, k) attachments of `pool` (round robin,
+ * epoch flip) and admit requests at k / t_x (router_set_admission).  Writes M
+ * to *m_out.  RING_EINVAL if the pool has fewer than M (or more than 8 are needed). */
+ring_status_t router_size_route(router_t r, uint32_t app_id, uint16_t stage, uint64_t t_x, uint64_t t_y, uint32_t k,
+                                const ring_peer_t* pool, uint32_t n_pool, uint32_t* m_out, void* stream);
 
 /* ---- misc ------------------------------------------------------------------------ */
 ring_status_t ring_set_timeout_ns(uint64_t ns);

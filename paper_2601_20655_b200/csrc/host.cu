@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "ring_internal.h"
+#include "ring_stage.cuh"
 
 using namespace b200ring;
 
@@ -116,6 +117,8 @@ ring_status_t crc_table_dev(int device, const uint32_t** out) {
     CUDA_TRY(preload_put());
     CUDA_TRY(preload_get());
     CUDA_TRY(preload_clock());
+    CUDA_TRY(preload_stage());
+    CUDA_TRY(preload_fanin());
     g_crc_dev[device] = d;
   }
   *out = g_crc_dev[device];
@@ -173,6 +176,8 @@ struct ring_peer_s {
   uint64_t* trace = nullptr;                 // debug timeline (B200RING_TRACE=1)
   const uint32_t* crc = nullptr;
   FaultSpec fault;                           // test-only fault injection (fault-tolerant rings)
+  void* stage_ctl = nullptr;                 // grid-coordination block of fused puts (ring_stage.cuh)
+  uint32_t launches_stage = 0;
 };
 
 struct router_s {
@@ -205,6 +210,7 @@ const char* ring_strerror(ring_status_t s) {
     case RING_EPEER: return "no peer access / IPC failure";
     case RING_EPENDING: return "pending";
     case RING_EDROPPED: return "dropped: size slot taken after a lock take-over";
+    case RING_EREJECTED: return "rejected by admission control";
   }
   return "unknown";
 }
@@ -453,6 +459,7 @@ ring_status_t ring_detach(ring_peer_t p) {
   cudaFree(p->desc_dev);
   cudaFree(p->ctx);
   cudaFree(p->st);
+  if (p->stage_ctl) cudaFree(p->stage_ctl);
   delete p;
   return RING_OK;
 }
@@ -468,6 +475,105 @@ ring_status_t ring_peer_config(ring_peer_t p, uint32_t copy_ctas, uint32_t threa
 }
 
 uint64_t ring_peer_submitted(ring_peer_t p) { return p ? p->base : 0; }
+
+// ---- lock-free fan-in set (fanin.cu) -----------------------------------------------
+struct SetRingHost {                         // layout of fanin.cu's SetRing
+  uint8_t* ring;
+  uint8_t* data;
+  uint64_t** mirrors;
+  uint64_t R;
+  uint32_t N;
+  uint32_t _p;
+};
+struct ring_set_s {
+  int device = 0;
+  uint32_t k = 0;
+  bool sys = false;
+  void* rings_dev = nullptr;
+  const uint32_t* crc = nullptr;
+  uint32_t rr = 0;
+};
+
+ring_status_t ring_set_create(const ring_t* rings, uint32_t n, ring_set_t* out) {
+  if (!rings || !out || n == 0 || n > 32) return RING_EINVAL;
+  std::vector<SetRingHost> h(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    ring_t r = rings[i];
+    if (!r || r->device != rings[0]->device) return RING_EINVAL;
+    h[i] = SetRingHost{r->base, r->base + r->data_off, r->mirrors_dev, r->R, r->N, 0};
+  }
+  ring_set_s* s = new ring_set_s;
+  s->device = rings[0]->device;
+  s->k = n;
+  for (uint32_t i = 0; i < n; ++i) s->sys = s->sys || rings[i]->sys;
+  DevGuard g(s->device);
+  CUDA_TRY(cudaMalloc(&s->rings_dev, sizeof(SetRingHost) * n));
+  CUDA_TRY(cudaMemcpy(s->rings_dev, h.data(), sizeof(SetRingHost) * n, cudaMemcpyHostToDevice));
+  ring_status_t st = crc_table_dev(s->device, &s->crc);
+  if (st != RING_OK) return st;
+  *out = s;
+  return RING_OK;
+}
+
+ring_status_t ring_set_destroy(ring_set_t s) {
+  if (!s) return RING_EINVAL;
+  DevGuard g(s->device);
+  cudaDeviceSynchronize();
+  cudaFree(s->rings_dev);
+  delete s;
+  return RING_OK;
+}
+
+ring_status_t ring_set_consume(ring_set_t s, uint32_t n, ring_view_t* d_views, uint32_t* d_ring_idx, uint32_t flags,
+                               void* stream) {
+  if (!s || !d_views || n == 0) return RING_EINVAL;
+  DevGuard g(s->device);
+  CUDA_TRY(launch_set_consume(static_cast<const SetRing*>(s->rings_dev), s->k, d_views, d_ring_idx, n, s->crc, flags,
+                              g_timeout_ns, s->rr, s->sys, as_stream(stream)));
+  s->rr = (s->rr + 1) % s->k;
+  g_launches++;
+  return RING_OK;
+}
+
+ring_status_t ring_peer_device_view(ring_peer_t p, ring_dev_peer_t* out) {
+  if (!p || !out || p->desc.mpsc) return RING_EINVAL;
+  DevGuard g(p->device);
+  if (!p->stage_ctl) {
+    CUDA_TRY(cudaMalloc(&p->stage_ctl, sizeof(stage::StageCtl)));
+    CUDA_TRY(cudaMemset(p->stage_ctl, 0, sizeof(stage::StageCtl)));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  memset(out, 0, sizeof *out);
+  out->ring = reinterpret_cast<uint64_t>(p->desc.ring);
+  out->data = reinterpret_cast<uint64_t>(p->desc.data);
+  out->state = reinterpret_cast<uint64_t>(p->st);
+  out->ctl = reinterpret_cast<uint64_t>(p->stage_ctl);
+  out->crc_table = reinterpret_cast<uint64_t>(p->crc);
+  out->R = p->desc.R;
+  out->N = p->desc.N;
+  out->producer_id = p->desc.producer_id;
+  out->sys = p->desc.sys;
+  return RING_OK;
+}
+
+ring_status_t ring_stage_scale_bf16_put(ring_peer_t p, const void* d_in, uint64_t n_elems, float scale,
+                                        const ring_hdr_t* hdr, uint32_t flags, uint32_t* d_status, void* stream) {
+  if (!p || !d_in || !hdr || !d_status || hdr->reserved) return RING_EINVAL;
+  ring_dev_peer_t v;
+  ring_status_t s = ring_peer_device_view(p, &v);
+  if (s != RING_OK) return s;
+  DevGuard g(p->device);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+  const uint64_t work = (n_elems + 7) / 8;
+  const uint32_t ctas = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm * 2, (work + 255) / 256));
+  CUDA_TRY(launch_stage_scale_put(v, d_in, n_elems, scale, *hdr, flags, d_status, g_timeout_ns, ctas,
+                                  as_stream(stream)));
+  p->launches_stage++;
+  p->base += 1;
+  g_launches++;
+  return RING_OK;
+}
 
 ring_status_t ring_peer_set_fault(ring_peer_t p, const ring_fault_t* f) {
   if (!p || !p->desc.ft) return RING_EINVAL;
@@ -748,6 +854,44 @@ ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, cons
   CUDA_TRY(cudaMemcpyAsync(&d->dests, &staged.dests, sizeof(staged.dests), cudaMemcpyHostToDevice, as_stream(stream)));
   CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
   return RING_OK;
+}
+
+ring_status_t router_set_admission(router_t r, uint32_t app_id, uint16_t stage, uint64_t t_x, uint32_t k,
+                                   void* stream) {
+  if (!r || (k && t_x == 0)) return RING_EINVAL;
+  uint32_t slot = r->max_routes;
+  for (uint32_t i = 0; i < r->max_routes; ++i)
+    if (r->routes[i].n && r->routes[i].app_id == app_id && r->routes[i].stage == stage) { slot = i; break; }
+  if (slot == r->max_routes) return RING_EINVAL;
+  DevGuard g(r->device);
+  static thread_local Route staged;
+  staged.adm_tx = t_x;
+  staged.adm_k = k;
+  staged._ra = 0;
+  staged.adm_next = 0;
+  Route* d = r->routes_dev + slot;
+  const size_t off = offsetof(Route, adm_tx);
+  CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(d) + off, reinterpret_cast<uint8_t*>(&staged) + off,
+                           sizeof(Route) - off, cudaMemcpyHostToDevice, as_stream(stream)));
+  CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+  return RING_OK;
+}
+
+uint64_t ring_required_instances(uint64_t t_x, uint64_t t_y, uint32_t k) {
+  if (t_x == 0 || t_y == 0 || k == 0) return 0;
+  const unsigned __int128 num = (unsigned __int128)k * t_y;
+  return (uint64_t)((num + t_x - 1) / t_x);
+}
+
+ring_status_t router_size_route(router_t r, uint32_t app_id, uint16_t stage, uint64_t t_x, uint64_t t_y, uint32_t k,
+                                const ring_peer_t* pool, uint32_t n_pool, uint32_t* m_out, void* stream) {
+  const uint64_t m = ring_required_instances(t_x, t_y, k);
+  if (!r || !pool || m == 0 || m > n_pool || m > kMaxDests) return RING_EINVAL;
+  ring_status_t s = router_set_route(r, app_id, stage, pool, (uint32_t)m, stream);
+  if (s != RING_OK) return s;
+  s = router_set_admission(r, app_id, stage, t_x, k, stream);
+  if (s == RING_OK && m_out) *m_out = (uint32_t)m;
+  return s;
 }
 
 ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, uint32_t flags, uint32_t* d_status,

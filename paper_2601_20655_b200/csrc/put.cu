@@ -79,6 +79,7 @@ struct MsgBrief {        // the fields lane 0 needs, computed in parallel by all
   uint32_t stage;
   uint32_t nunits;       // copy work units
   uint32_t _p;
+  uint64_t t_arr;        // arrival time (hdr.accepted_at): fast-reject admission
 };
 
 __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, LeaderState& L, uint32_t k0,
@@ -99,15 +100,26 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
     // ---- stage router (PAPER.md:531-532 round-robin; epoch = reassignment)
     uint32_t d = 0;
     int hit = -1;
+    uint64_t adm_next = 0;   // admission state to commit with the message
     if (a.routes) {
       for (uint32_t r = 0; r < a.n_routes; ++r)
         if (a.routes[r].n && a.routes[r].app_id == m.app_id && a.routes[r].stage == m.stage) { hit = (int)r; break; }
       if (hit < 0) {
         o.status = RING_EINVAL;
       } else {
-        const Route& rt = a.routes[hit];
+        Route& rt = a.routes[hit];
         d = rt.dests[rt.rr % rt.n];
         o.epoch = rt.epoch;
+        // Request Monitor / fast reject: admitted iff the
+        // arrival is not earlier than the next admissible time (rate K/T_X,
+        // burst 1, the oracle's pipeline.fast_reject); rejected requests are
+        // never sent and leave the round robin where it was.
+        adm_next = rt.adm_next;
+        if (rt.adm_k) {
+          const uint64_t t = m.t_arr * rt.adm_k;
+          if (t >= rt.adm_next) adm_next = max(rt.adm_next, t) + rt.adm_tx;
+          else o.status = RING_EREJECTED;
+        }
       }
     }
     const DestDesc D = dests[d];
@@ -214,9 +226,14 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
     L.tails[d] = P;
     if (defer) { done_l = l; break; }
     if (o.status == RING_ETIMEDOUT) L.aborted = true;
-    if (hit >= 0) a.routes[hit].rr = a.routes[hit].rr + 1;   // committed: advance the round robin
-    o.seq = (uint32_t)L.chans[d];
-    L.chans[d] += 1;
+    if (hit >= 0 && o.status != RING_EREJECTED) {   // committed: advance the round robin and the admission
+      a.routes[hit].rr = a.routes[hit].rr + 1;
+      a.routes[hit].adm_next = adm_next;
+    }
+    if (o.status != RING_EREJECTED) {   // a rejected request never reaches the channel
+      o.seq = (uint32_t)L.chans[d];
+      L.chans[d] += 1;
+    }
     o.item = L.items++;
     o.flags = kStatus | (o.status == RING_OK ? kEntry : 0u);
     if (o.status == RING_OK) {
@@ -555,6 +572,7 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
       brief[lane].app_id = mp->hdr.app_id;
       brief[lane].stage = mp->hdr.stage;
       brief[lane].nunits = units_for(len, a.chunk);
+      brief[lane].t_arr = mp->hdr.accepted_at;
     }
     uint64_t tc = 0, cq = 0;   // issued together with the brief loads (first round)
     if (lane == 0 && fast && !(L.loaded & 1u)) {

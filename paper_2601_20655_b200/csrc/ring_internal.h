@@ -125,6 +125,13 @@ struct Route {
   uint32_t epoch;
   uint32_t rr;          // round-robin counter (device-owned)
   uint32_t dests[kMaxDests];
+  // Fast reject: admit at rate adm_k / adm_tx (burst 1) by
+  // arrival time hdr.accepted_at; adm_next = next admissible time * adm_k
+  // (exact integer arithmetic).  adm_k == 0: no admission control.
+  uint64_t adm_tx;
+  uint32_t adm_k;
+  uint32_t _ra;
+  uint64_t adm_next;    // device-owned
 };
 
 struct PutArgs {
@@ -191,6 +198,15 @@ cudaError_t launch_release(const ReleaseArgs& a, cudaStream_t s);
 cudaError_t preload_put();
 cudaError_t preload_get();
 cudaError_t preload_clock();
+cudaError_t preload_stage();
+cudaError_t preload_fanin();
+struct SetRing;
+cudaError_t launch_set_consume(const SetRing* rings, uint32_t k, ring_view_t* views, uint32_t* ring_idx, uint32_t n,
+                               const uint32_t* crc, uint32_t flags, uint64_t timeout_ns, uint32_t rr, bool sys,
+                               cudaStream_t s);
+cudaError_t launch_stage_scale_put(const ring_dev_peer_t& peer, const void* in, uint64_t n, float scale,
+                                   const ring_hdr_t& hdr, uint32_t flags, uint32_t* status, uint64_t timeout_ns,
+                                   uint32_t ctas, cudaStream_t s);
 cudaError_t launch_clock_publish(unsigned long long* mapped_host, unsigned long long duration_ns, cudaStream_t s);
 
 }  // namespace b200ring

@@ -19,8 +19,9 @@ LIB_PATH = os.path.join(_HERE, "libb200ring.so")
 # ---- status codes / flags (include/b200ring.h) ------------------------------------
 RING_OK, RING_EINVAL, RING_ENOMEM, RING_EMSGSIZE, RING_FULL, RING_EMPTY = 0, 1, 2, 3, 4, 5
 RING_ETIMEDOUT, RING_ECORRUPT, RING_ECUDA, RING_EPEER, RING_EPENDING, RING_EDROPPED = 6, 7, 8, 9, 10, 11
+RING_EREJECTED = 12
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EMSGSIZE", 4: "FULL", 5: "EMPTY", 6: "ETIMEDOUT",
-                7: "ECORRUPT", 8: "ECUDA", 9: "EPEER", 10: "EPENDING", 11: "EDROPPED"}
+                7: "ECORRUPT", 8: "ECUDA", 9: "EPEER", 10: "EPENDING", 11: "EDROPPED", 12: "EREJECTED"}
 RING_BLOCK, RING_TRY, RING_NO_TIMESTAMP = 0, 1, 2
 RING_CREATE_DEFAULT, RING_CREATE_LOCAL, RING_CREATE_FAULT_TOLERANT = 0, 1, 2
 RING_AT_LOCK, RING_AT_GH, RING_AT_WB, RING_AT_WL, RING_AT_UH = 1, 2, 3, 4, 5
@@ -39,6 +40,12 @@ class ring_handle_t(C.Structure):
 class ring_fault_t(C.Structure):
     _fields_ = [("die_after", C.c_uint32), ("pause_mask", C.c_uint32), ("msg", C.c_uint32),
                 ("reserved", C.c_uint32), ("arrived", C.c_void_p), ("go", C.c_void_p)]
+
+
+class ring_dev_peer_t(C.Structure):
+    _fields_ = [("ring", C.c_uint64), ("data", C.c_uint64), ("state", C.c_uint64), ("ctl", C.c_uint64),
+                ("crc_table", C.c_uint64), ("R", C.c_uint64), ("N", C.c_uint32), ("producer_id", C.c_uint32),
+                ("sys", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class ring_info_t(C.Structure):
@@ -96,6 +103,13 @@ def _load():
         "ring_peer_trace": [P, P, U32],
         "ring_peer_set_fault": [P, C.POINTER(ring_fault_t)],
         "ring_set_lock_timeout_ns": [U64],
+        "router_set_admission": [P, U32, C.c_uint16, U64, U32, P],
+        "ring_peer_device_view": [P, C.POINTER(ring_dev_peer_t)],
+        "ring_set_create": [C.POINTER(P), U32, C.POINTER(P)],
+        "ring_set_destroy": [P],
+        "ring_set_consume": [P, U32, P, P, U32, P],
+        "ring_stage_scale_bf16_put": [P, P, U64, C.c_float, C.POINTER(ring_hdr_t), U32, P, P],
+        "router_size_route": [P, U32, C.c_uint16, U64, U64, U32, C.POINTER(P), U32, C.POINTER(U32), P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -111,6 +125,8 @@ def _load():
     lib.ring_footprint.restype = C.c_uint64
     lib.ring_peer_submitted.argtypes = [P]
     lib.ring_peer_submitted.restype = C.c_uint64
+    lib.ring_required_instances.argtypes = [U64, U64, U32]
+    lib.ring_required_instances.restype = C.c_uint64
     return lib
 
 
@@ -328,3 +344,56 @@ def ring_peer_set_fault(peer: int, die_after: int = 0, pause_mask: int = 0, msg:
 
 def ring_set_lock_timeout_ns(ns: int) -> None:
     _check("ring_set_lock_timeout_ns", lib.ring_set_lock_timeout_ns(int(ns)))
+
+
+# ---- pipeline sizing / admission --------------------------------
+def router_set_admission(router: int, app_id: int, stage: int, t_x: int, k: int, stream=None) -> None:
+    _check("router_set_admission", lib.router_set_admission(router, app_id, stage, int(t_x), int(k), _stream(stream)))
+
+
+def ring_required_instances(t_x: int, t_y: int, k: int) -> int:
+    return int(lib.ring_required_instances(int(t_x), int(t_y), int(k)))
+
+
+def router_size_route(router: int, app_id: int, stage: int, t_x: int, t_y: int, k: int, pool, stream=None) -> int:
+    arr = (C.c_void_p * len(pool))(*pool)
+    m = C.c_uint32()
+    _check("router_size_route", lib.router_size_route(router, app_id, stage, int(t_x), int(t_y), int(k), arr,
+                                                      len(pool), C.byref(m), _stream(stream)))
+    return m.value
+
+
+# ---- fused device-side put -----------------------------------------
+def ring_peer_device_view(peer: int) -> dict:
+    v = ring_dev_peer_t()
+    _check("ring_peer_device_view", lib.ring_peer_device_view(peer, C.byref(v)))
+    return {name: getattr(v, name) for name, _ in ring_dev_peer_t._fields_}
+
+
+def ring_stage_scale_bf16_put(peer: int, d_in, n_elems: int, scale: float, uid: bytes = bytes(16),
+                              accepted_at: int = 0, app_id: int = 0, stage: int = 0, flags: int = 0,
+                              d_status=None, stream=None) -> None:
+    """Synthetic stage with a fused put epilogue: out = bf16(in * scale) written
+    by the computing kernel straight into the peer ring (one message)."""
+    h = ring_hdr_t()
+    C.memmove(h.uid, bytes(uid), 16)
+    h.accepted_at, h.app_id, h.stage, h.reserved = accepted_at, app_id, stage, 0
+    _check("ring_stage_scale_bf16_put", lib.ring_stage_scale_bf16_put(peer, _ptr(d_in), int(n_elems), float(scale),
+                                                                      C.byref(h), flags, _ptr(d_status),
+                                                                      _stream(stream)))
+
+
+# ---- lock-free fan-in set (SURVEY.md sec 8 f3) -----------------------------------------
+def ring_set_create(rings) -> int:
+    arr = (C.c_void_p * len(rings))(*rings)
+    out = C.c_void_p()
+    _check("ring_set_create", lib.ring_set_create(arr, len(rings), C.byref(out)))
+    return out.value
+
+
+def ring_set_destroy(s: int) -> None:
+    _check("ring_set_destroy", lib.ring_set_destroy(s))
+
+
+def ring_set_consume(s: int, n: int, d_views, d_ring_idx=None, flags: int = 0, stream=None) -> None:
+    _check("ring_set_consume", lib.ring_set_consume(s, n, _ptr(d_views), _ptr(d_ring_idx), flags, _stream(stream)))
