@@ -152,8 +152,11 @@ def run_pipeline(args, rank, world, grp, offsets):
 
 def run_fanin(args, rank, world, grp, offsets):
     dev = torch.cuda.current_device()
-    plan = T.plan_fanin(world, 1 << 30, 256)
+    lockfree = getattr(args, "fanin_mode", "mpsc") == "set"
+    plan = T.plan_fanin_set(world, 512 << 20, 256) if lockfree else T.plan_fanin(world, 1 << 30, 256)
     wired = _wire(plan, rank, world, grp, dev)
+    my_ring = f"sub{rank}" if lockfree else "fan0"
+    rset = R.ring_set_create([wired.rings[f"sub{p}"] for p in range(1, world)]) if lockfree and rank == 0 else None
     sizes = [4096 << (2 * i) for i in range(9)]          # 4 KiB .. 256 MiB
     if args.sizes:
         sizes = [int(x) for x in args.sizes.split(",")]
@@ -174,9 +177,12 @@ def run_fanin(args, rank, world, grp, offsets):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
             if rank == 0:
-                R.ring_consume(wired.rings["fan0"], total, vt, None, 0, 0, s)
+                if lockfree:
+                    R.ring_set_consume(rset, total, vt, None, 0, s)
+                else:
+                    R.ring_consume(wired.rings["fan0"], total, vt, None, 0, 0, s)
             else:
-                R.ring_put_batch(wired.peers["fan0"], d_msgs, M, 0, st, s)
+                R.ring_put_batch(wired.peers[my_ring], d_msgs, M, 0, st, s)
             e1.record(s)
             torch.cuda.synchronize()
             res = [e0.elapsed_time(e1)]
@@ -200,16 +206,22 @@ def run_fanin(args, rank, world, grp, offsets):
                      "msgs_per_s": round(M * (world - 1) / (ms / 1e3), 1),
                      "lat_p50_us": _pct(lat0, 50), "lat_p99_us": _pct(lat0, 99), "lat_samples": len(lat0),
                      "ok": float(t[1]) == 0.0})
+    if rset is not None:
+        R.ring_set_destroy(rset)
     _teardown(wired, grp)
     if rank != 0:
         return None
     best = max(r["ingress_gbs"] for r in rows)
-    return {"metric": METRIC, "topology": "fanin", "value": best, "unit": "GB/s", "n_gpus": world,
+    return {"metric": METRIC, "topology": "fanin" + ("-set" if lockfree else ""), "value": best, "unit": "GB/s",
+            "n_gpus": world, "fanin_mode": "lock-free: one SPSC ring per producer, one consumer warp" if lockfree
+            else "paper MPSC ring with the lock",
             "producers": world - 1, "sweep": rows,
             "roofline": {"bound": "nvlink (consumer ingress)", "achieved": best, "peak": NVLINK_PEAK_MEASURED,
                          "frac": round(best / NVLINK_PEAK_MEASURED, 4)},
-            "config": {"workload": "C5a: GPUs 1..N-1 -> one MPSC ring (paper lock) on GPU 0, size sweep",
-                       "R_bytes": 1 << 30, "n_slots": 256},
+            "config": {"workload": ("C5a variant (SURVEY.md sec 8 f3): GPUs 1..N-1 -> one 512 MiB SPSC ring each on GPU 0, "
+                                    "one consumer warp" if lockfree else
+                                    "C5a: GPUs 1..N-1 -> one MPSC ring (paper lock) on GPU 0, size sweep"),
+                       "R_bytes": (512 << 20) if lockfree else 1 << 30, "n_slots": 256},
             "higher_is_better": True, "dtype": "u8", "data": "synthetic"}
 
 

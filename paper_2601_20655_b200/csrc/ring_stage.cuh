@@ -113,6 +113,10 @@ __device__ void commit_one(const ring_dev_peer_t& p, uint64_t P, uint64_t len, c
   st->chan_seq = st->chan_seq + 1;
 }
 
+// A reservation as returned to the stage's threads: the tail word at the
+// entry with bit 63 set (tail offsets are < 2^39, so bit 63 is free); 0 = none.
+constexpr uint64_t kReserved = 1ull << 63;
+
 // Grid-wide protocol for a fused stage kernel writing ONE message:
 //   const uint64_t P = grid_reserve(p, ctl, len, timeout);   // every thread
 //   ... write payload bytes at payload_ptr(p, P) ...
@@ -126,10 +130,10 @@ __device__ uint64_t grid_reserve(const ring_dev_peer_t& p, StageCtl* ctl, uint64
     uint64_t P = 0;
     if (blockIdx.x == 0) {
       const uint32_t s = reserve_one<SYS>(p, len, timeout_ns, &P);
-      ctl->P = s == RING_OK ? P : 0;
+      P = s == RING_OK ? (P | kReserved) : 0;
+      ctl->P = P;
       ctl->status = s;
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&ctl->ready), "r"(1u) : "memory");
-      if (s != RING_OK) P = 0;
     } else {
       const uint64_t t0 = globaltimer();
       while (ld_acquire_gpu32(&ctl->ready) == 0u)
@@ -143,7 +147,7 @@ __device__ uint64_t grid_reserve(const ring_dev_peer_t& p, StageCtl* ctl, uint64
 }
 
 __device__ __forceinline__ uint8_t* payload_ptr(const ring_dev_peer_t& p, uint64_t P) {
-  return reinterpret_cast<uint8_t*>(p.data) + ptr_off(P) + kHdr;
+  return reinterpret_cast<uint8_t*>(p.data) + ptr_off(P & ~kReserved) + kHdr;
 }
 
 template <bool SYS>
@@ -156,7 +160,7 @@ __device__ void grid_commit(const ring_dev_peer_t& p, StageCtl* ctl, uint64_t P,
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctl->done) : "memory");
     if (prev + 1 == gridDim.x) {            // last CTA: every payload store is ordered before this point
       const uint32_t s = ctl->status;
-      if (s == RING_OK && P) commit_one<SYS>(p, P, len, h, flags);
+      if (s == RING_OK && P) commit_one<SYS>(p, P & ~kReserved, len, h, flags);
       if (status) *status = s;
       ctl->ready = 0;                       // reset for the next stream-ordered launch
       ctl->done = 0;

@@ -94,6 +94,17 @@ def plan_fanin(world: int, data_bytes: int = 1 << 30, n_slots: int = 256, spare_
     return w
 
 
+def plan_fanin_set(world: int, data_bytes: int = 512 << 20, n_slots: int = 256) -> Wiring:
+    """Lock-free fan-in: one single-producer ring per
+    producer rank 1..world-1, all owned by rank 0 (served by ring_set_consume)."""
+    assert world >= 2
+    w = Wiring()
+    for p in range(1, world):
+        w.rings.append(RingSpec(f"sub{p}", 0, data_bytes, n_slots, 1))
+        w.attach.append(Attach(p, f"sub{p}", 0))
+    return w
+
+
 @dataclass
 class Wired:
     rings: dict            # name -> ring handle (rings this rank owns)
