@@ -48,9 +48,14 @@ def _views(vt):
     return R.parse_views(vt.cpu().numpy())
 
 
-def _lat_us(v, off_cons, off_prod_by_id):
+def _lat_us(v, off_cons, off_prod_by_id, by_ring=False):
+    """t_visible - t_put on the host clock; the producer is the header's
+    producer id, or (ring sets, every ring's producer has id 0) the ring index."""
     t_put = np.frombuffer(v["header"][:, 56:64].tobytes(), dtype="<u8").astype(np.int64)
-    pid = np.frombuffer(v["header"][:, 44:48].tobytes(), dtype="<u4").astype(np.int64)
+    if by_ring:
+        pid = v["reserved"][:, 0].astype(np.int64)
+    else:
+        pid = np.frombuffer(v["header"][:, 44:48].tobytes(), dtype="<u4").astype(np.int64)
     offp = np.array([off_prod_by_id[int(p)] for p in pid], dtype=np.int64)
     return (((v["t_visible"].astype(np.int64) - off_cons) - (t_put - offp)) / 1e3).tolist()
 
@@ -191,7 +196,7 @@ def run_fanin(args, rank, world, grp, offsets):
         if rank == 0:
             v = _views(vt)
             ok = bool((v["status"] == 0).all())
-            lat = _lat_us(v, offsets[0], {p - 1: offsets[p] for p in range(1, world)})
+            lat = _lat_us(v, offsets[0], {p - 1: offsets[p] for p in range(1, world)}, by_ring=lockfree)
         else:
             ok = bool((st == 0).all().item())
         t = torch.tensor([res[0], 0.0 if ok else 1.0], dtype=torch.float64)
