@@ -262,14 +262,18 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
 // position against the cached head; the leading run of lanes that fit is
 // placed.  Returns the run length; 0 leaves the round to the serial path
 // (credit wait, second wrap, EMSGSIZE).
-__device__ uint32_t fast_place(const PutArgs& a, LaunchCtx* ctx, LeaderState& L, uint32_t gmax, GroupSlot* gs,
-                               const MsgBrief* brief, const DestDesc& D) {
+// The placement rule of one round, per lane (also evaluated by every CTA at
+// launch start to start copies before the leader's plans arrive, see
+// SpecRound): a pure function of the tail P, the head H and the lengths.
+struct RoundPlace {
+  uint64_t start, tail_after, pad_start;
+  uint32_t seq, item_off, fu_off, nu, run, w, pad_seq, nu_total;
+  bool pad_used, c;
+};
+__device__ __forceinline__ RoundPlace place_round(uint64_t P, uint64_t H, bool act, uint64_t f, uint32_t nu_in,
+                                                  const DestDesc& D) {
   const int lane = threadIdx.x & 31;
-  const bool act = (uint32_t)lane < gmax;
-  const uint64_t f = act ? brief[lane].f : 0;
-  const uint64_t len = act ? brief[lane].len : 0;
-  if (__ballot_sync(0xffffffffu, act && (len >= (1ull << 32) || f > D.R))) return 0;
-  const uint64_t P = L.tails[0], H = L.heads[0];
+  RoundPlace r;
   const uint64_t pb = ptr_off(P), hb = ptr_off(H);
   const uint32_t pq = ptr_seq(P), hq = ptr_seq(H);
   const uint64_t incl = warp_incl_scan64(f, lane);
@@ -295,32 +299,60 @@ __device__ uint32_t fast_place(const PutArgs& a, LaunchCtx* ctx, LeaderState& L,
     ok = ok && seq_dist(pad_seq, hq) < D.N && span_free(pad_start, pad_seq, hb, hq, D.R - pad_start);
   const uint32_t notok = __ballot_sync(0xffffffffu, !ok);
   const uint32_t run = notok ? (uint32_t)__ffs(notok) - 1 : 32u;
+  r.run = run;
+  r.pad_used = has_pad && w < run;
+  r.c = (uint32_t)lane < run;
+  r.nu = r.c ? nu_in : 0;
+  const uint32_t nu_incl = warp_incl_scan32(r.nu, lane);
+  r.fu_off = nu_incl - r.nu;
+  r.nu_total = __shfl_sync(0xffffffffu, nu_incl, 31);
+  r.start = start;
+  r.seq = seq;
+  r.item_off = lane + ((r.pad_used && (uint32_t)lane >= w) ? 1 : 0);
+  r.tail_after = pack_ptr(advance(start, f, D.R), seq_inc(seq));
+  r.w = w;
+  r.pad_start = pad_start;
+  r.pad_seq = pad_seq;
+  return r;
+}
+
+__device__ uint32_t fast_place(const PutArgs& a, LaunchCtx* ctx, LeaderState& L, uint32_t gmax, GroupSlot* gs,
+                               const MsgBrief* brief, const DestDesc& D) {
+  const int lane = threadIdx.x & 31;
+  const bool act = (uint32_t)lane < gmax;
+  const uint64_t f = act ? brief[lane].f : 0;
+  const uint64_t len = act ? brief[lane].len : 0;
+  if (__ballot_sync(0xffffffffu, act && (len >= (1ull << 32) || f > D.R))) return 0;
+  const RoundPlace r = place_round(L.tails[0], L.heads[0], act, f, act ? brief[lane].nunits : 0, D);
+  const uint32_t run = r.run;
   if (run == 0) return 0;
-  const bool pad_used = has_pad && w < run;
-  const bool c = (uint32_t)lane < run;
-  const uint32_t nu = c ? brief[lane].nunits : 0;
-  const uint32_t nu_incl = warp_incl_scan32(nu, lane);
+  const bool pad_used = r.pad_used;
+  const bool c = r.c;
+  const uint32_t nu = r.nu;
   const uint32_t items0 = L.items, units0 = L.units;
   const uint64_t chan0 = L.chans[0];
-  const uint64_t tail_after = pack_ptr(advance(start, f, D.R), seq_inc(seq));
+  const uint64_t tail_after = r.tail_after;
+  const uint64_t start = r.start;
+  const uint32_t seq = r.seq, w = r.w, pad_seq = r.pad_seq;
+  const uint64_t pad_start = r.pad_start;
   if (c) {
     GroupSlot o = {};
     o.start = start;
     o.slot = seq;
     o.tail_after = tail_after;
-    o.item = items0 + lane + ((pad_used && (uint32_t)lane >= w) ? 1 : 0);
+    o.item = items0 + r.item_off;
     o.dest = 0;
     o.seq = (uint32_t)(chan0 + lane);
     o.status = RING_OK;
     o.flags = kStatus | kEntry;
     o.nunits = nu;
-    o.first_unit = units0 + nu_incl - nu;
+    o.first_unit = units0 + r.fu_off;
     gs[lane] = o;
   }
   if (pad_used && (uint32_t)lane == w)
     write_pad_plan(ctx, items0 + w, 0, pad_seq, kBusy | kPad | (D.R - pad_start), pack_ptr(0, seq_inc(pad_seq)));
   const uint64_t last_tail = __shfl_sync(0xffffffffu, tail_after, run - 1);
-  const uint32_t nu_total = __shfl_sync(0xffffffffu, nu_incl, 31);
+  const uint32_t nu_total = r.nu_total;
   __syncwarp();
   if (lane == 0) {
     L.items = items0 + run + (pad_used ? 1 : 0);
@@ -636,7 +668,6 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
         p.seq = o.seq;
         p.epoch = o.epoch;
       }
-      S->arrive[o.item % kPlanRing] = 0;   // item o.item - kPlanRing is published (flow control)
       if (a.dest_out) a.dest_out[k] = o.dest;
     }
     __syncwarp();
@@ -798,6 +829,9 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
     if (pend && dest0 != pend_dest) flush();
     const DestDesc& D = a.dests[dest0];
     const bool mine = (uint32_t)lane < run;
+    // the counter is reused by item j + kPlanRing, planned only after pub_seq passes j
+    // (reset even without units: a speculative copy may have counted into it)
+    if (mine) S->arrive[j % kPlanRing] = 0;
     if (mine && (flags & kEntry) && D.mpsc) {   // WL: size + busy bit (PAD entries carry the pad bit)
       if (D.sys) st_relaxed<true>(slot_w(D, slot), slot_word);
       else st_relaxed<false>(slot_w(D, slot), slot_word);
@@ -827,6 +861,60 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
     if (!full || unlock_now || run < 32 || pend_n >= 96) flush();
   }
   if (pend) flush();
+}
+
+// One warp per CTA: the first kSpecRounds rounds' placement as the leader will
+// decide it (place_round on the producer-local tail and a fresh head; round r
+// starts from round r-1's last tail, as the leader's does), into shared memory
+// for the CTA's copy warps.  n_units = 0 when not applicable.
+__device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
+  const int lane = threadIdx.x & 31;
+  const DestDesc& D = a.dest0;
+  // not under RING_TRY: an aborted message would shift every later placement
+  const bool fast = !a.routes && a.n_dests == 1 && !D.mpsc && !D.ft && a.copy_mode == 0 && a.msgs &&
+                    !(a.flags & RING_TRY);
+  if (!fast) {
+    if (lane == 0) { sp->n_units = 0; sp->n = 0; }
+    return;
+  }
+  uint64_t P = 0, H = 0;
+  if (lane == 0) {
+    P = __ldcg(reinterpret_cast<const unsigned long long*>(&D.st->tail_cache));
+    H = read_head(D);
+  }
+  P = __shfl_sync(0xffffffffu, P, 0);
+  H = __shfl_sync(0xffffffffu, H, 0);
+  uint32_t n_msgs = 0, units = 0, items = 0;
+  for (int rnd = 0; rnd < kSpecRounds; ++rnd) {
+    const uint32_t k0 = rnd * kGroup;
+    if (k0 >= a.n) break;
+    const uint32_t gmax = min((uint32_t)kGroup, a.n - k0);
+    const bool act = (uint32_t)lane < gmax;
+    uint64_t len = 0, src = 0;
+    if (act) { len = a.msgs[k0 + lane].len; src = a.msgs[k0 + lane].src; }
+    const uint64_t f = act ? footprint(len) : 0;
+    if (__ballot_sync(0xffffffffu, act && (len >= (1ull << 32) || f > D.R))) break;   // the leader goes serial
+    const RoundPlace r = place_round(P, H, act, f, act ? units_for(len, a.chunk) : 0, D);
+    if (r.c) {
+      SpecItem& it = sp->it[k0 + lane];
+      it.src = src;
+      it.dst = reinterpret_cast<uint64_t>(D.data + r.start + kHdr);
+      it.len = len;
+      it.first_unit = units + r.fu_off;
+      it.nunits = r.nu;
+      it.item = items + r.item_off;
+    }
+    n_msgs = k0 + r.run;
+    units += r.nu_total;
+    items += r.run + (r.pad_used ? 1u : 0u);
+    if (r.run < (uint32_t)kGroup) break;                 // the next round starts elsewhere (credit)
+    P = __shfl_sync(0xffffffffu, r.tail_after, 31);
+  }
+  if (lane == 0) { sp->n = n_msgs; sp->n_units = n_msgs ? units : 0; }
+  if (a.trace && lane == 0 && blockIdx.x == 1) {
+    a.trace[1880] = sp->n_units; a.trace[1881] = n_msgs; a.trace[1882] = H; a.trace[1883] = P;
+    a.trace[1884] = globaltimer();
+  }
 }
 
 __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
@@ -859,7 +947,13 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
     if (warp == (blockIdx.x == 0 ? 2 : 0)) copy_engine<kEngineStages>(ctx, S, a.chunk, a.timeout_ns, dyn_smem);
     return;
   }
-  copy_warp(ctx, S, &cs, a.chunk, a.timeout_ns, a.trace);
+  // the CTA's first copy warp evaluates the first round; the copy warps meet
+  // on named barrier 2 (CTA 0's control warps never wait for it)
+  __shared__ SpecRound spec;
+  const uint32_t ncopy = blockDim.x - (blockIdx.x == 0 ? 64u : 0u);
+  if (warp == (blockIdx.x == 0 ? 2 : 0)) spec_first_round(a, &spec);
+  asm volatile("bar.sync 2, %0;" ::"r"(ncopy) : "memory");
+  copy_warp(ctx, S, &cs, a.chunk, a.timeout_ns, a.trace, &spec);
 }
 
 // With CUDA's lazy module loading, the first launch of a kernel loads it, and

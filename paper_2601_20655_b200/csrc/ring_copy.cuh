@@ -108,34 +108,63 @@ __device__ __forceinline__ uint64_t wait_planned(LaunchSet* S, CopyShared* cs, u
 // lanes read 32 candidate plans' copy sectors (unit range AND copy fields) in
 // one round trip; the hit lane broadcasts its fields.
 __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShared* cs, uint32_t chunk,
-                                          uint64_t timeout_ns, uint64_t* trace = nullptr) {
+                                          uint64_t timeout_ns, uint64_t* trace = nullptr,
+                                          const SpecRound* spec = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t cur = 0;   // items before `cur` hold no unit this warp can still take
+  // First unit: the warp's index among the grid's copy warps (CTA 0 keeps two
+  // control warps), no atomic -- ~1,000 warps taking their first unit with an
+  // atomicAdd on one word serialise for microseconds.  Later units: dynamic.
+  const uint32_t wpc = blockDim.x >> 5;
+  const uint32_t n_static = gridDim.x * wpc - 2;
+  uint32_t first = blockIdx.x == 0 ? (threadIdx.x >> 5) - 2 : (wpc - 2) + (blockIdx.x - 1) * wpc + (threadIdx.x >> 5);
+  bool have_first = true;
   // debug timeline: the first unit of the first copy warp of each CTA
   uint64_t* tr = (trace && (threadIdx.x >> 5) == (blockIdx.x == 0 ? 2 : 0)) ? trace + 1280 + 4 * blockIdx.x : nullptr;
   while (true) {
     uint32_t u = 0, quit = 0, ps = 0;
     if (lane == 0) {
       if (tr) tr[0] = globaltimer();
-      u = atomicAdd(&S->next_unit, 1u);
-      bool to = false;
-      const uint64_t pl = wait_planned(S, cs, u, timeout_ns, to);
-      if (to || planned_units(pl) <= u) {
-        quit = 1;
-        if (trace) atomicMax(reinterpret_cast<unsigned long long*>(trace + 254), (unsigned long long)globaltimer());
+      u = have_first ? first : n_static + atomicAdd(&S->next_unit, 1u);
+      if (!(spec && u < spec->n_units)) {      // not covered by the CTA's speculative first round
+        bool to = false;
+        const uint64_t pl = wait_planned(S, cs, u, timeout_ns, to);
+        if (to || planned_units(pl) <= u) {
+          quit = 1;
+          if (trace) atomicMax(reinterpret_cast<unsigned long long*>(trace + 254), (unsigned long long)globaltimer());
+        }
+        ps = planned_items(pl);
       }
-      ps = planned_items(pl);
       if (tr) tr[1] = globaltimer();
     }
     __syncwarp();
+    have_first = false;
     quit = __shfl_sync(0xffffffffu, quit, 0);
     if (quit) return;
     u = __shfl_sync(0xffffffffu, u, 0);
     ps = __shfl_sync(0xffffffffu, ps, 0);
-    // find the item holding unit u (plans are read through L2: ring slots are reused)
     uint32_t item = 0xffffffffu, fu = 0;
     uint64_t src = 0, dst = 0, len = 0;
-    for (uint32_t b = cur; b < ps; b += 32) {
+    if (spec && u < spec->n_units) {           // the CTA's own evaluation of the first rounds (shared memory)
+      for (uint32_t b = 0; b < spec->n; b += 32) {
+        const uint32_t i = b + lane;
+        const bool in = i < spec->n;
+        const SpecItem& si = spec->it[in ? i : 0];
+        const bool hit = in && si.nunits && u >= si.first_unit && u - si.first_unit < si.nunits;
+        const uint32_t m = __ballot_sync(0xffffffffu, hit);
+        if (m) {
+          const SpecItem& sh = spec->it[b + __ffs(m) - 1];
+          item = sh.item;
+          fu = sh.first_unit;
+          src = sh.src;
+          dst = sh.dst;
+          len = sh.len;
+          break;
+        }
+      }
+    }
+    // find the item holding unit u (plans are read through L2: ring slots are reused)
+    for (uint32_t b = cur; item == 0xffffffffu && b < ps; b += 32) {
       const uint32_t i = b + lane;
       bool hit = false;
       ulonglong2 q0 = make_ulonglong2(0, 0), q1 = make_ulonglong2(0, 0);

@@ -77,6 +77,27 @@ struct alignas(64) Plan {
 static_assert(sizeof(Plan) == 192, "Plan layout");
 static_assert(offsetof(Plan, nunits) == 28, "copy fields in the first sector");
 
+// Speculative first round (put, single SPSC destination): every CTA evaluates
+// the leader's placement rule for the launch's first <= 32 messages from the
+// producer-local tail and its own snapshot of the head, so its copy warps can
+// start before the leader's plans arrive.  Placement does not depend on the
+// head (only *whether* an entry fits does, and the head only moves forward):
+// every entry that fits for the CTA fits identically for the leader.
+struct SpecItem {
+  uint64_t src, dst, len;
+  uint32_t first_unit, nunits, item, _p;
+};
+#ifndef B200RING_SPEC_ROUNDS
+#define B200RING_SPEC_ROUNDS 1
+#endif
+constexpr int kSpecRounds = B200RING_SPEC_ROUNDS;   // leader rounds evaluated speculatively
+struct SpecRound {
+  uint32_t n_units;     // units [0, n_units) are described by it[]
+  uint32_t n;           // messages described
+  uint32_t _p[2];
+  SpecItem it[kSpecRounds * kGroup];
+};
+
 // Per-CTA cache of the launch's `planned` word for the copy warps: one warp
 // at a time polls the global word (gpu-scope acquire) and republishes it in
 // shared memory (cta-scope release), so ~one poller per SM instead of one per

@@ -112,9 +112,13 @@ for ctas in grids:
                     rounds = [(rel(h[4*r]), rel(h[4*r+1]), rel(h[4*r+2])) for r in range(4) if h[4*r]]
                     fl = [(rel(h[256+2*j]), int(h[257+2*j])) for j in range(8) if h[256+2*j]]
                     cw = [h[1280 + 4*b + 1] for b in range(148) if h[1280 + 4*b + 1]]
+                    cg = [h[1280 + 4*b + 0] for b in range(148) if h[1280 + 4*b + 0]]
+                    print(f"      {nm}: copy grab {rel(min(cg)) if cg else None}-{rel(max(cg)) if cg else None}; "
+                          f"cta1 grab/planned/found/done {[rel(h[1280 + 4 + k]) for k in range(4)]}")
                     cf = [h[1280 + 4*b + 2] for b in range(148) if h[1280 + 4*b + 2]]
                     cd = [h[1280 + 4*b + 3] for b in range(148) if h[1280 + 4*b + 3]]
-                    print(f"      {nm}: copy-warp last exit {rel(h[254])}")
+                    print(f"      {nm}: copy-warp last exit {rel(h[254])} spec(cta1): units {h[1880]} run {h[1881]} "
+                          f"H {h[1882] >> 24}/{h[1882] & 0xffffff} P {h[1883] >> 24}/{h[1883] & 0xffffff} at {rel(h[1884])}")
                     print(f"      {nm}: entry {rel(h[252])} rounds(start,placed,hdr) {rounds} copies planned "
                           f"{rel(min(cw)) if cw else None}-{rel(max(cw)) if cw else None} found {rel(min(cf)) if cf else None}-{rel(max(cf)) if cf else None} "
                           f"done {rel(min(cd)) if cd else None}-{rel(max(cd)) if cd else None} flushes {fl} end {rel(h[253])}")
