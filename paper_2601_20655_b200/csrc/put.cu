@@ -668,6 +668,12 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
         p.seq = o.seq;
         p.epoch = o.epoch;
       }
+      // An arrive counter is reused by item + kPlanRing, planned only once
+      // pub_seq has passed the item (flow control); the first kPlanRing items
+      // start from the zeroed set, and the speculative first round only ever
+      // counts into those.  (No reset in the publisher: its flush fence then
+      // has nothing left to wait for.)
+      if (o.item >= (uint32_t)kPlanRing) S->arrive[o.item % kPlanRing] = 0;
       if (a.dest_out) a.dest_out[k] = o.dest;
     }
     __syncwarp();
@@ -829,9 +835,6 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
     if (pend && dest0 != pend_dest) flush();
     const DestDesc& D = a.dests[dest0];
     const bool mine = (uint32_t)lane < run;
-    // the counter is reused by item j + kPlanRing, planned only after pub_seq passes j
-    // (reset even without units: a speculative copy may have counted into it)
-    if (mine) S->arrive[j % kPlanRing] = 0;
     if (mine && (flags & kEntry) && D.mpsc) {   // WL: size + busy bit (PAD entries carry the pad bit)
       if (D.sys) st_relaxed<true>(slot_w(D, slot), slot_word);
       else st_relaxed<false>(slot_w(D, slot), slot_word);
