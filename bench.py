@@ -569,8 +569,9 @@ def main():
     ap.add_argument("--topology", default="pairs", choices=["pairs", "pipeline", "fanin", "reassign"],
                     help="N>1: pairs (default bench line) or the C4 / C5a / C5b runs of bench_multi.py")
     ap.add_argument("--sizes", default="", help="fanin: comma-separated message sizes")
-    ap.add_argument("--fanin-mode", default="mpsc", choices=["mpsc", "set"],
-                    help="fanin: the paper's locked MPSC ring, or one SPSC ring per producer + ring_set_consume")
+    ap.add_argument("--fanin-mode", default="mpsc", choices=["mpsc", "set", "rc"],
+                    help="fanin: the paper's locked MPSC ring, one SPSC ring per producer + ring_set_consume, "
+                         "or a reserve-then-commit MPSC ring")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--lat-iters", type=int, default=40)
     ap.add_argument("--no-overlap", action="store_true", help="N=1: put(s+1) waits for consume(s)")

@@ -76,7 +76,7 @@ def _fill(nbytes, seed):
 
 def _wire(plan, rank, world, grp, dev):
     return T.wire(plan, rank, world, grp, device=dev,
-                  create=lambda s, d: R.ring_create(d, s.data_bytes, s.n_slots, s.max_producers, 0),
+                  create=lambda s, d: R.ring_create(d, s.data_bytes, s.n_slots, s.max_producers, s.flags),
                   export=R.ring_export, attach=R.ring_attach_peer, bind=R.ring_bind_mirror)
 
 
@@ -157,8 +157,10 @@ def run_pipeline(args, rank, world, grp, offsets):
 
 def run_fanin(args, rank, world, grp, offsets):
     dev = torch.cuda.current_device()
-    lockfree = getattr(args, "fanin_mode", "mpsc") == "set"
-    plan = T.plan_fanin_set(world, 512 << 20, 256) if lockfree else T.plan_fanin(world, 1 << 30, 256)
+    mode = getattr(args, "fanin_mode", "mpsc")
+    lockfree = mode == "set"
+    plan = T.plan_fanin_set(world, 512 << 20, 256) if lockfree else \
+        T.plan_fanin(world, 1 << 30, 256, flags=R.RING_CREATE_RESERVE_COMMIT if mode == "rc" else 0)
     wired = _wire(plan, rank, world, grp, dev)
     my_ring = f"sub{rank}" if lockfree else "fan0"
     rset = R.ring_set_create([wired.rings[f"sub{p}"] for p in range(1, world)]) if lockfree and rank == 0 else None
@@ -217,9 +219,11 @@ def run_fanin(args, rank, world, grp, offsets):
     if rank != 0:
         return None
     best = max(r["ingress_gbs"] for r in rows)
-    return {"metric": METRIC, "topology": "fanin" + ("-set" if lockfree else ""), "value": best, "unit": "GB/s",
-            "n_gpus": world, "fanin_mode": "lock-free: one SPSC ring per producer, one consumer warp" if lockfree
-            else "paper MPSC ring with the lock",
+    return {"metric": METRIC, "topology": "fanin" + ("-" + mode if mode != "mpsc" else ""), "value": best,
+            "unit": "GB/s", "n_gpus": world,
+            "fanin_mode": {"set": "lock-free: one SPSC ring per producer, one consumer warp",
+                           "rc": "reserve-then-commit MPSC ring: claim under the lock, copy outside it",
+                           "mpsc": "paper MPSC ring with the lock"}[mode],
             "producers": world - 1, "sweep": rows,
             "roofline": {"bound": "nvlink (consumer ingress)", "achieved": best, "peak": NVLINK_PEAK_MEASURED,
                          "frac": round(best / NVLINK_PEAK_MEASURED, 4)},

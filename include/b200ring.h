@@ -74,6 +74,16 @@ typedef enum {
  * Slot words gain a 22-bit sequence tag in bits 40-61 (R21).  Each message is
  * appended with the sender's steps one at a time (no batching of publishes). */
 #define RING_CREATE_FAULT_TOLERANT 2u
+/* Reserve-then-commit MPSC: the lock guards only the
+ * claim -- under it a sender reads the reservation frontier and the head,
+ * applies the space rule, marks the size slot reserved (bit 61) with its
+ * footprint and advances the frontier -- and the payload is copied outside the
+ * lock, so producers of one ring copy concurrently; WL commits the slot
+ * (reserved -> busy) and any sender moves the tail over the leading run of
+ * committed slots (CAS), so entries are published in claim order.  The
+ * receiver is unchanged.  Senders must not be lost (a reservation that is
+ * never committed stalls the tail); combine with nothing else. */
+#define RING_CREATE_RESERVE_COMMIT 4u
 
 /* Geometry limits (R5, R8) */
 #define RING_ENTRY_ALIGN 128u

@@ -394,6 +394,7 @@ ring_status_t ring_attach_peer(const ring_handle_t* h, int producer_device, uint
   p->desc.N = b.N;
   p->desc.ft = (b.flags & RING_CREATE_FAULT_TOLERANT) ? 1u : 0u;
   p->desc.mpsc = (b.max_producers > 1 || p->desc.ft) ? 1u : 0u;   // fault tolerance needs the lock
+  p->desc.rc = ((b.flags & RING_CREATE_RESERVE_COMMIT) && p->desc.mpsc && !p->desc.ft) ? 1u : 0u;
   p->desc.producer_id = producer_id;
   p->desc.has_mirror = 0;
   p->desc.sys = (same_process && producer_device == b.device) ? 0u : 1u;

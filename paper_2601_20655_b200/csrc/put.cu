@@ -28,6 +28,7 @@ namespace b200ring {
 __device__ __forceinline__ uint64_t* lock_w(const DestDesc& d) { return reinterpret_cast<uint64_t*>(d.ring + kLockOff); }
 __device__ __forceinline__ uint64_t* tail_w(const DestDesc& d) { return reinterpret_cast<uint64_t*>(d.ring + kTailOff); }
 __device__ __forceinline__ uint64_t* head_w(const DestDesc& d) { return reinterpret_cast<uint64_t*>(d.ring + kHeadOff); }
+__device__ __forceinline__ uint64_t* resv_w(const DestDesc& d) { return reinterpret_cast<uint64_t*>(d.ring + kResvOff); }
 __device__ __forceinline__ uint64_t* slot_w(const DestDesc& d, uint32_t q) {
   return reinterpret_cast<uint64_t*>(d.ring + kSlotsOff) + (q & (d.N - 1));
 }
@@ -142,7 +143,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
     if (o.status == RING_OK && D.mpsc && !locked) {
       // Step 1 "Acquire the lock using a CAS-based spinlock",
       // after our own previous items (and their Unlock) are published.
-      while (ld_acquire_gpu32(&S->pub_seq) != L.items)
+      while (!D.rc && ld_acquire_gpu32(&S->pub_seq) != L.items)   // RC: the leader unlocks itself
         if (globaltimer() - t_start > a.timeout_ns) { o.status = RING_ETIMEDOUT; break; }
       if (o.status == RING_OK) {
         const uint64_t me = (uint64_t)D.producer_id + 1;
@@ -152,7 +153,13 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
           if (globaltimer() - t_start > a.timeout_ns) { o.status = RING_ETIMEDOUT; break; }
         }
       }
-      if (locked) {
+      if (locked && D.rc) {
+        // reserve-then-commit: claim from the reservation frontier (entries
+        // between the tail and it are reserved or committed, not lost)
+        P = D.sys ? ld_relaxed<true>(resv_w(D)) : ld_relaxed<false>(resv_w(D));
+        L.heads[d] = read_head(D);
+        held = (int)d;
+      } else if (locked) {
         // Step 2: read the tail (ordered after the acquiring CAS).
         P = D.sys ? ld_relaxed<true>(tail_w(D)) : ld_relaxed<false>(tail_w(D));
         // Step 4 (R6, before the space check): a busy slot at P_seq with the
@@ -182,6 +189,10 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         if (!full && pb + f > D.R) {
           if (span_free(pb, pq, hb, hq, D.R - pb)) {
             const uint64_t P2 = pack_ptr(0, seq_inc(pq));
+            if (D.rc) {   // a PAD is claimed and committed at once (nothing to copy)
+              if (D.sys) { st_relaxed<true>(slot_w(D, pq), kBusy | kPad | (D.R - pb)); st_relaxed<true>(resv_w(D), P2); }
+              else { st_relaxed<false>(slot_w(D, pq), kBusy | kPad | (D.R - pb)); st_relaxed<false>(resv_w(D), P2); }
+            }
             write_pad_plan(ctx, L.items, d, pq, kBusy | kPad | (D.R - pb), P2);
             last_pad = L.items;
             L.items++;
@@ -198,6 +209,10 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
           o.slot = pq;
           P = pack_ptr(advance(pb, f, D.R), seq_inc(pq));
           o.tail_after = P;
+          if (D.rc) {   // claim: reserved slot + frontier, under the lock
+            if (D.sys) { st_relaxed<true>(slot_w(D, pq), kResvBit | f); st_relaxed<true>(resv_w(D), P); }
+            else { st_relaxed<false>(slot_w(D, pq), kResvBit | f); st_relaxed<false>(resv_w(D), P); }
+          }
           break;
         }
         // Not enough credit with the cached head: re-read it once.
@@ -243,7 +258,13 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
     }
     gs[l] = o;
   }
-  if (held >= 0) {
+  if (held >= 0 && dests[held].rc) {
+    // reserve-then-commit: the claims are done -- unlock now (release orders
+    // the reserved slots and the frontier before it); copies and commits
+    // happen outside the lock
+    const DestDesc& D = dests[held];
+    if (D.sys) st_release<true>(lock_w(D), 0ull); else st_release<false>(lock_w(D), 0ull);
+  } else if (held >= 0) {
     // Step 8 "Release the lock" after the round's LAST item (a PAD planned
     // for a deferred message comes after the last message item).
     if (last_pad == L.items - 1) ctx->plan[last_pad % kPlanRing].flags |= kUnlock;
@@ -835,6 +856,54 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
     if (pend && dest0 != pend_dest) flush();
     const DestDesc& D = a.dests[dest0];
     const bool mine = (uint32_t)lane < run;
+    if (D.rc) {
+      // Reserve-then-commit (oracle/reserve.py): WL commits each reserved slot
+      // (reserved -> busy, after the copies: fence), then the tail moves over
+      // the leading run of committed slots -- ours or another sender's.
+      if (pend) flush();
+      if (D.sys) fence_acq_rel<true>(); else fence_acq_rel<false>();
+      if (mine && (flags & kEntry) && !(slot_word & kPad))
+        dcas(D, slot_w(D, slot), kResvBit | (slot_word & ((1ull << 40) - 1)), slot_word);
+      __syncwarp();
+      {
+        // warp-parallel: the lanes read up to 32 slots from the tail, the
+        // leading run of committed ones (entries tile the ring, PADs fill
+        // every wrap: offsets add mod R) moves the tail with ONE CAS
+        uint64_t T = 0, Rv = 0, H = 0;
+        if (lane == 0) { T = dld(D, tail_w(D)); Rv = dld(D, resv_w(D)); H = read_head(D); }
+        T = __shfl_sync(0xffffffffu, T, 0);
+        Rv = __shfl_sync(0xffffffffu, Rv, 0);
+        H = __shfl_sync(0xffffffffu, H, 0);
+        while (true) {
+          const uint32_t tq = ptr_seq(T);
+          const uint32_t room = D.N - min(D.N, seq_dist(tq, ptr_seq(H)));
+          const uint32_t k = min(min(seq_dist(ptr_seq(Rv), tq), room), 32u);
+          uint64_t w = 0;
+          if ((uint32_t)lane < k) w = dld(D, slot_w(D, (tq + lane) & kSeqMask));
+          const uint32_t notbusy = __ballot_sync(0xffffffffu, !((uint32_t)lane < k && (w & kBusy)));
+          const uint32_t nrun = notbusy ? __ffs(notbusy) - 1 : 32u;
+          if (nrun == 0) break;                             // the tail's slot is reserved, not committed yet
+          const uint64_t fsum = warp_sum64((uint32_t)lane < nrun ? (w & ((1ull << 40) - 1)) : 0);
+          const uint64_t T2 = pack_ptr((ptr_off(T) + fsum) % D.R, tq + nrun);
+          uint64_t old = 0;
+          if (lane == 0) old = dcas(D, tail_w(D), T, T2);
+          old = __shfl_sync(0xffffffffu, old, 0);
+          T = old == T ? T2 : old;                           // moved (look further) or somebody else did
+        }
+        if (lane == 0) st_u32_relaxed_gpu(&S->pub_seq, i + run);
+      }
+      i += run;
+      const uint32_t srcl = min((uint32_t)lane + run, 31u);
+      const bool hv = __shfl_sync(0xffffffffu, have, srcl) && (uint32_t)lane + run < 32;
+      flags = __shfl_sync(0xffffffffu, flags, srcl);
+      dest = __shfl_sync(0xffffffffu, dest, srcl);
+      nunits = __shfl_sync(0xffffffffu, nunits, srcl);
+      slot = __shfl_sync(0xffffffffu, slot, srcl);
+      slot_word = __shfl_sync(0xffffffffu, slot_word, srcl);
+      tail_after = __shfl_sync(0xffffffffu, tail_after, srcl);
+      have = hv;
+      continue;
+    }
     if (mine && (flags & kEntry) && D.mpsc) {   // WL: size + busy bit (PAD entries carry the pad bit)
       if (D.sys) st_relaxed<true>(slot_w(D, slot), slot_word);
       else st_relaxed<false>(slot_w(D, slot), slot_word);

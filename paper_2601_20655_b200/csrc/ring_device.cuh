@@ -24,6 +24,8 @@ constexpr uint64_t kHdr = 64;        // entry header bytes (R11)
 constexpr uint64_t kBusy = 1ull << 63;
 constexpr uint64_t kPad = 1ull << 62;
 constexpr uint64_t kFMask = (1ull << 62) - 1;
+constexpr uint64_t kResvBit = 1ull << 61;   // reserve-then-commit: slot claimed, entry not committed yet
+constexpr uint64_t kResvOff = 64;          // reservation frontier word (lock line; written under the lock)
 constexpr uint32_t kSeqMask = (1u << 24) - 1;
 constexpr int kPlanRing = 128;       // in-flight items (entries) per launch context
 constexpr int kGroup = 32;           // messages planned per leader round (one per lane)

@@ -39,6 +39,8 @@ struct DestDesc {
   uint32_t has_mirror;   // unused by the kernels (mirror validity is in-band)
   uint32_t sys;          // 1: ring / consumer on another GPU -> .sys scope
   uint32_t ft;           // RING_CREATE_FAULT_TOLERANT: take-over, CAS WL/UH/Unlock, tags, payload CRC
+  uint32_t rc;           // RING_CREATE_RESERVE_COMMIT: claim under the lock, copy and commit outside it
+  uint32_t _pad2;
 };
 
 // Test-only fault injection of a put launch (ring_peer_set_fault).

@@ -23,7 +23,7 @@ RING_EREJECTED = 12
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EMSGSIZE", 4: "FULL", 5: "EMPTY", 6: "ETIMEDOUT",
                 7: "ECORRUPT", 8: "ECUDA", 9: "EPEER", 10: "EPENDING", 11: "EDROPPED", 12: "EREJECTED"}
 RING_BLOCK, RING_TRY, RING_NO_TIMESTAMP = 0, 1, 2
-RING_CREATE_DEFAULT, RING_CREATE_LOCAL, RING_CREATE_FAULT_TOLERANT = 0, 1, 2
+RING_CREATE_DEFAULT, RING_CREATE_LOCAL, RING_CREATE_FAULT_TOLERANT, RING_CREATE_RESERVE_COMMIT = 0, 1, 2, 4
 RING_AT_LOCK, RING_AT_GH, RING_AT_WB, RING_AT_WL, RING_AT_UH = 1, 2, 3, 4, 5
 RING_HDR_BYTES, RING_ENTRY_ALIGN = 64, 128
 

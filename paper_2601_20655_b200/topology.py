@@ -32,6 +32,7 @@ class RingSpec:
     data_bytes: int
     n_slots: int
     max_producers: int = 1
+    flags: int = 0         # ring_create flags (e.g. reserve-then-commit)
 
 
 @dataclass(frozen=True)
@@ -80,10 +81,11 @@ def plan_pipeline(world: int, hop_bytes: list[int], hop_slots: list[int]) -> Wir
     return w
 
 
-def plan_fanin(world: int, data_bytes: int = 1 << 30, n_slots: int = 256, spare_consumer: bool = False) -> Wiring:
+def plan_fanin(world: int, data_bytes: int = 1 << 30, n_slots: int = 256, spare_consumer: bool = False,
+               flags: int = 0) -> Wiring:
     assert world >= 2
     w = Wiring()
-    w.rings.append(RingSpec("fan0", 0, data_bytes, n_slots, world - 1))
+    w.rings.append(RingSpec("fan0", 0, data_bytes, n_slots, world - 1, flags))
     for p in range(1, world):
         w.attach.append(Attach(p, "fan0", p - 1))
     if spare_consumer and world >= 3:
