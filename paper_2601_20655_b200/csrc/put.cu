@@ -943,8 +943,7 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
   const int lane = threadIdx.x & 31;
   const DestDesc& D = a.dest0;
   // not under RING_TRY: an aborted message would shift every later placement
-  const bool fast = !a.routes && a.n_dests == 1 && !D.mpsc && !D.ft && a.copy_mode == 0 && a.msgs &&
-                    !(a.flags & RING_TRY);
+  const bool fast = !a.routes && a.n_dests == 1 && !D.mpsc && !D.ft && a.msgs && !(a.flags & RING_TRY);
   if (!fast) {
     if (lane == 0) { sp->n_units = 0; sp->n = 0; }
     return;
@@ -989,6 +988,9 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
   }
 }
 
+// MODE 0: LSU copy warps; MODE 1: one TMA engine warp per CTA.  Two kernels,
+// so the TMA path's registers never change the LSU copy loop's code.
+template <int MODE>
 __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
   LaunchCtx* ctx = a.ctx;
   LaunchSet* S = &ctx->set[a.launch & 1];
@@ -1014,14 +1016,18 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
       return;
     }
   }
-  if (a.copy_mode == 1) {      // TMA engine: one warp per CTA (CTA 0: warp 2)
+  __shared__ SpecRound spec;
+  if (MODE == 1) {             // TMA engine: one warp per CTA (CTA 0: warp 2); it evaluates the first round itself
     extern __shared__ __align__(128) uint8_t dyn_smem[];
-    if (warp == (blockIdx.x == 0 ? 2 : 0)) copy_engine<kEngineStages>(ctx, S, a.chunk, a.timeout_ns, dyn_smem);
+    if (warp == (blockIdx.x == 0 ? 2 : 0)) {
+      spec_first_round(a, &spec);
+      __syncwarp();
+      copy_engine<kEngineStages>(ctx, S, a.chunk, a.timeout_ns, dyn_smem, &spec);
+    }
     return;
   }
   // the CTA's first copy warp evaluates the first round; the copy warps meet
   // on named barrier 2 (CTA 0's control warps never wait for it)
-  __shared__ SpecRound spec;
   const uint32_t ncopy = blockDim.x - (blockIdx.x == 0 ? 64u : 0u);
   if (warp == (blockIdx.x == 0 ? 2 : 0)) spec_first_round(a, &spec);
   asm volatile("bar.sync 2, %0;" ::"r"(ncopy) : "memory");
@@ -1034,15 +1040,17 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
 // times out; so every kernel is loaded when a device is first used.
 cudaError_t preload_put() {
   cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, put_kernel);
+  cudaError_t e = cudaFuncGetAttributes(&fa, put_kernel<0>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, put_kernel<1>);
   if (e == cudaSuccess)   // TMA engine stages (up to kEngineStages x 48 KiB)
-    e = cudaFuncSetAttribute(put_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kEngineStages * (48 << 10));
+    e = cudaFuncSetAttribute(put_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEngineStages * (48 << 10));
   return e;
 }
 
 cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s) {
   const size_t dyn = a.copy_mode == 1 ? (size_t)kEngineStages * a.chunk : 0;
-  put_kernel<<<ctas, a.copy_mode == 1 ? 96u : threads, dyn, s>>>(a);
+  if (a.copy_mode == 1) put_kernel<1><<<ctas, 96u, dyn, s>>>(a);
+  else put_kernel<0><<<ctas, threads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

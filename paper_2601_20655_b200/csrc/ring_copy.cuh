@@ -235,8 +235,29 @@ __device__ __forceinline__ uint32_t find_item(LaunchCtx* ctx, uint32_t u, uint32
   return 0xffffffffu;
 }
 
+// Unit u's (item, first unit, src, dst, len) from a CTA's speculative first
+// round, or item = 0xffffffff if not covered.
+__device__ __forceinline__ void spec_lookup(const SpecRound* spec, uint32_t u, int lane, uint32_t& item, uint32_t& fu,
+                                            uint64_t& src, uint64_t& dst, uint64_t& len) {
+  item = 0xffffffffu;
+  if (!spec || u >= spec->n_units) return;
+  for (uint32_t b = 0; b < spec->n; b += 32) {
+    const uint32_t i = b + lane;
+    const bool in = i < spec->n;
+    const SpecItem& si = spec->it[in ? i : 0];
+    const bool hit = in && si.nunits && u >= si.first_unit && u - si.first_unit < si.nunits;
+    const uint32_t m = __ballot_sync(0xffffffffu, hit);
+    if (m) {
+      const SpecItem& sh = spec->it[b + __ffs(m) - 1];
+      item = sh.item; fu = sh.first_unit; src = sh.src; dst = sh.dst; len = sh.len;
+      return;
+    }
+  }
+}
+
 template <int STAGES>
-__device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns, uint8_t* bufs) {
+__device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns, uint8_t* bufs,
+                            const SpecRound* spec = nullptr) {
   const int lane = threadIdx.x & 31;
   __shared__ __align__(8) uint64_t bar[STAGES];
   __shared__ EngineStage st[STAGES];
@@ -251,16 +272,23 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
   uint32_t pending_u = 0xffffffffu;         // unit taken but not planned yet
   bool exhausted = false;
   uint64_t wait_end = 0;
+  // the first STAGES units of every engine are static (strided over the grid:
+  // no atomic, low units first), later ones dynamic
+  uint32_t n_taken = 0;
+  const uint32_t n_static = (uint32_t)STAGES * gridDim.x;
   while (true) {
     // ---- refill free stages with planned units
     while (!exhausted && k_issue - k_done < (uint32_t)STAGES) {
       uint32_t u = 0, state = 0, ps = 0;    // state 0 = planned, 1 = not yet, 2 = exhausted
       if (lane == 0) {
-        if (pending_u == 0xffffffffu) pending_u = atomicAdd(&S->next_unit, 1u);
+        if (pending_u == 0xffffffffu)
+          pending_u = n_taken < (uint32_t)STAGES ? blockIdx.x + n_taken * gridDim.x : n_static + atomicAdd(&S->next_unit, 1u);
         u = pending_u;
-        const uint64_t pl = ld_acquire<false>(&S->planned);
-        if (planned_units(pl) <= u) state = planned_done(pl) ? 2 : 1;
-        else ps = planned_items(pl);
+        if (!(spec && u < spec->n_units)) {
+          const uint64_t pl = ld_acquire<false>(&S->planned);
+          if (planned_units(pl) <= u) state = planned_done(pl) ? 2 : 1;
+          else ps = planned_items(pl);
+        }
       }
       __syncwarp();
       state = __shfl_sync(0xffffffffu, state, 0);
@@ -277,12 +305,19 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
       u = __shfl_sync(0xffffffffu, u, 0);
       ps = __shfl_sync(0xffffffffu, ps, 0);
       pending_u = 0xffffffffu;
-      const uint32_t item = find_item(ctx, u, cur, ps, lane);
-      if (item == 0xffffffffu) { exhausted = true; break; }
-      cur = item;
-      const Plan& p = ctx->plan[item % kPlanRing];
-      const uint64_t src = ld_cg64(&p.src), dst = ld_cg64(&p.dst), len = ld_cg64(&p.len);
-      const uint32_t c = u - ld_cg32(&p.first_unit);
+      ++n_taken;
+      uint32_t item, fu = 0;
+      uint64_t src = 0, dst = 0, len = 0;
+      spec_lookup(spec, u, lane, item, fu, src, dst, len);
+      if (item == 0xffffffffu) {
+        item = find_item(ctx, u, cur, ps, lane);
+        if (item == 0xffffffffu) { exhausted = true; break; }
+        const Plan& p = ctx->plan[item % kPlanRing];
+        src = ld_cg64(&p.src); dst = ld_cg64(&p.dst); len = ld_cg64(&p.len);
+        fu = ld_cg32(&p.first_unit);
+        cur = item;
+      }
+      const uint32_t c = u - fu;
       const uint64_t lo = (uint64_t)c * chunk;
       const uint64_t hi = min(len, lo + chunk);
       const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src) + lo;
