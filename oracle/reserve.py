@@ -13,9 +13,14 @@ forward over the leading run of busy slots (a CAS per step), so entries are
 published in claim order whoever finishes first.  The receiver is unchanged
 (PAPER.md:709-718).
 
-Slot words: busy << 63 | pad << 62 | resv << 61 | f.  Fault-free model (a
-lost reservation would stall the tail; liveness under sender failure is the
-fault-tolerant ring's business, oracle/fault.py).  Shares no code with the
+Slot words: busy << 63 | pad << 62 | resv << 61 | f.
+
+A sender waits (helping) until the tail has passed its own entry.  With
+`crash=True` one sender may be lost at any point; a sender spinning on a lock
+held by the lost one takes it over (TL), and a sender whose
+entry waits behind the lost one's reservation turns that hole into a PAD
+(reserved -> busy|pad, a CAS; on the GPU after the same timeout TL): the
+receiver skips it and liveness is kept.  Shares no code with the
 product path.
 """
 from __future__ import annotations
@@ -30,13 +35,14 @@ F40 = (1 << 40) - 1
 
 
 class RCProducer:
-    __slots__ = ("pid", "msgs", "k", "pc", "p_b", "p_q", "f", "seen_head")
+    __slots__ = ("pid", "msgs", "k", "pc", "p_b", "p_q", "f", "seen_head", "dead")
 
     def __init__(self, pid, msgs):
         self.pid, self.msgs, self.k = pid, msgs, 0
         self.pc = "Lock" if msgs else "DONE"
         self.p_b = self.p_q = self.f = 0
         self.seen_head = None
+        self.dead = False
 
     def clone(self):
         c = RCProducer.__new__(RCProducer)
@@ -45,12 +51,14 @@ class RCProducer:
         return c
 
     def key(self):
-        return (self.k, self.pc, self.p_b, self.p_q, self.f, self.seen_head)
+        return (self.k, self.pc, self.p_b, self.p_q, self.f, self.seen_head, self.dead)
 
 
 class RCSim:
-    def __init__(self, L: Layout, programs: dict[int, list[Msg]], depth: int = 1):
+    def __init__(self, L: Layout, programs: dict[int, list[Msg]], depth: int = 1, crash: bool = False):
         self.L = L
+        self.crashes_left = 1 if crash else 0
+        self.resv_owner: dict[int, int] = {}       # slot seq -> claiming sender (bookkeeping)
         self.programs = programs
         self.lock = 0
         self.tail = 0
@@ -69,6 +77,7 @@ class RCSim:
     def clone(self):
         c = RCSim.__new__(RCSim)
         c.L, c.programs, c.depth = self.L, self.programs, self.depth
+        c.crashes_left, c.resv_owner = self.crashes_left, dict(self.resv_owner)
         c.lock, c.tail, c.head, c.resv = self.lock, self.tail, self.head, self.resv
         c.slots = list(self.slots)
         c.data = bytearray(self.data)
@@ -82,7 +91,8 @@ class RCSim:
 
     def key(self):
         return (self.lock, self.tail, self.head, self.resv, tuple(self.slots), bytes(self.data), tuple(self.owner),
-                tuple(p.key() for p in self.prods.values()), self.g_b, self.g_q, tuple(self.held), len(self.got))
+                tuple(p.key() for p in self.prods.values()), self.g_b, self.g_q, tuple(self.held),
+                tuple(self.got), self.crashes_left)
 
     # -- enabled actions ---------------------------------------------------------
     def _can_advance(self) -> bool:
@@ -94,17 +104,38 @@ class RCSim:
         _, r_q = unpack(self.resv)
         return t_q != r_q and used_slots(t_q, h_q) < self.L.N and bool(self.slots[t_q % self.L.N] & BUSY)
 
+    def _published(self, q: int) -> bool:
+        _, t_q = unpack(self.tail)
+        return 1 <= used_slots(t_q, q) < (1 << 23)        # the tail is past q (24-bit sequence distance)
+
+    def _hole(self):
+        """The tail's slot is reserved by a lost sender."""
+        _, t_q = unpack(self.tail)
+        _, r_q = unpack(self.resv)
+        w = self.slots[t_q % self.L.N]
+        if t_q == r_q or not (w & RESV):
+            return None
+        o = self.resv_owner.get(t_q)
+        return t_q if o is not None and self.prods[o].dead else None
+
     def enabled(self) -> list:
         acts = []
         for pid, p in self.prods.items():
-            if p.pc == "DONE":
+            if p.pc == "DONE" or p.dead:
                 continue
+            if self.crashes_left:
+                acts.append(("crash", pid))
             if p.pc == "Lock" and self.lock != 0:
+                if self.prods[self.lock - 1].dead:
+                    acts.append(("TL", pid))              # take over a lost sender's lock
                 continue
-            if p.pc == "RH" and self.head == p.seen_head:
-                continue
+            if p.pc == "RH" and self.head == p.seen_head and not self._can_advance() and self._hole() is None:
+                continue                                  # (a committed entry or a hole at the tail also wakes it)
             if p.pc in ("Adv", "AdvW") and not self._can_advance():
-                acts.append(("fin", pid))                 # nothing more to publish: next message / wait
+                if self._hole() is not None:
+                    acts.append(("fill", pid))            # reservation of a lost sender -> PAD
+                elif p.pc == "AdvW" or self._published(p.p_q):
+                    acts.append(("fin", pid))             # own entry published: next message / wait
                 continue
             acts.append(("step", pid))
         _, t_q = unpack(self.tail)
@@ -116,7 +147,7 @@ class RCSim:
 
     def done(self) -> bool:
         _, t_q = unpack(self.tail)
-        return all(p.pc == "DONE" for p in self.prods.values()) and t_q == self.g_q and not self.held
+        return all(p.pc == "DONE" or p.dead for p in self.prods.values()) and t_q == self.g_q and not self.held
 
     def step(self, act) -> str:
         kind, pid = act
@@ -124,6 +155,19 @@ class RCSim:
             lab = self._get()
         elif kind == "rel":
             lab = self._release()
+        elif kind == "crash":
+            self.prods[pid].dead = True
+            self.crashes_left -= 1
+            lab = f"crash({pid})"
+        elif kind == "TL":
+            self.lock = pid + 1
+            self.prods[pid].pc = "Claim"
+            lab = f"TL->Lock({pid})"
+        elif kind == "fill":
+            q = self._hole()
+            w = self.slots[q % self.L.N]
+            self.slots[q % self.L.N] = BUSY | PADBIT | (w & F40)
+            lab = f"Fill({pid})"
         elif kind == "fin":
             p = self.prods[pid]
             if p.pc == "AdvW":                            # published what it could: wait for credit
@@ -152,6 +196,18 @@ class RCSim:
             p.pc = "Claim"
             return f"Lock({me})"
         if p.pc == "Claim":
+            q = self._hole()
+            if q is not None:                             # a lost sender's reservation at the tail -> PAD
+                w = self.slots[q % L.N]
+                self.slots[q % L.N] = BUSY | PADBIT | (w & F40)
+                return f"Fill({me})"
+            if self._can_advance():
+                # like GH's repair (Case 7): first publish committed entries a
+                # sender left unpublished (e.g. lost right after its commit)
+                t_b, t_q = unpack(self.tail)
+                w = self.slots[t_q % L.N]
+                self.tail = pack(adv(L, t_b, w & F40), seq_next(t_q))
+                return f"UH({me})"
             # steps 2-4 on the reservation frontier (space rule R4, PAD R3)
             p.p_b, p.p_q = unpack(self.resv)
             h_b, h_q = unpack(self.head)
@@ -175,6 +231,7 @@ class RCSim:
             assert self.slots[p.p_q % L.N] == 0, "claimed slot not free"
             self._claim_units(p.p_b, p.f, (me, p.k))
             self.slots[p.p_q % L.N] = RESV | p.f
+            self.resv_owner[p.p_q] = me
             self.resv = pack(adv(L, p.p_b, p.f), seq_next(p.p_q))
             p.pc = "Unlock"
             return f"Claim({me})"
@@ -195,9 +252,9 @@ class RCSim:
             self.data[p.p_b + L.hdr: p.p_b + L.hdr + m.length] = m.payload
             p.pc = "WL"
             return f"WB({me})"
-        if p.pc == "WL":                                  # commit: reserved -> busy
+        if p.pc == "WL":                                  # commit: CAS reserved -> busy
             s = p.p_q % L.N
-            assert self.slots[s] == RESV | p.f
+            assert self.slots[s] == RESV | p.f, "a live sender's reservation was taken"
             self.slots[s] = BUSY | p.f
             p.pc = "Adv"
             return f"WL({me})"
@@ -244,13 +301,17 @@ class RCResult:
     violations: list = field(default_factory=list)
 
 
-def explore_rc(L: Layout, programs: dict, depth: int = 1, max_states: int = 2_000_000) -> RCResult:
+def explore_rc(L: Layout, programs: dict, depth: int = 1, max_states: int = 2_000_000,
+               crash: bool = False) -> RCResult:
     """Every interleaving: no claim over a live entry, the tail only moves over
     committed slots (each receive finds a busy slot and a valid header), every
-    channel delivered exactly once in order, no deadlock."""
+    channel delivered exactly once in order, no deadlock.  With `crash`, one
+    sender may be lost anywhere: the others still finish and the lost one's
+    channel is an in-order prefix of its messages (the one it was appending
+    when lost is delivered only if it had committed it)."""
     res = RCResult()
     seen = set()
-    stack = [RCSim(L, programs, depth)]
+    stack = [RCSim(L, programs, depth, crash)]
     while stack:
         s = stack.pop()
         k = s.key()
@@ -264,8 +325,10 @@ def explore_rc(L: Layout, programs: dict, depth: int = 1, max_states: int = 2_00
             res.terminals += 1
             for pid, msgs in programs.items():
                 mine = [(k2, pay) for p2, k2, pay in s.got if p2 == pid]
-                if [k2 for k2, _ in mine] != list(range(len(msgs))) or \
-                        any(pay != bytes(msgs[k2].payload) for k2, pay in mine):
+                ks = [k2 for k2, _ in mine]
+                pr = s.prods[pid]
+                want = [list(range(len(msgs)))] if not pr.dead else [list(range(pr.k)), list(range(pr.k + 1))]
+                if ks not in want or any(pay != bytes(msgs[k2].payload) for k2, pay in mine):
                     res.violations.append(("delivery", pid, s.log))
             continue
         acts = s.enabled()
