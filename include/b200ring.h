@@ -80,9 +80,13 @@ typedef enum {
  * footprint and advances the frontier -- and the payload is copied outside the
  * lock, so producers of one ring copy concurrently; WL commits the slot
  * (reserved -> busy) and any sender moves the tail over the leading run of
- * committed slots (CAS), so entries are published in claim order.  The
- * receiver is unchanged.  Senders must not be lost (a reservation that is
- * never committed stalls the tail); combine with nothing else. */
+ * committed slots (CAS), so entries are published in claim order; a put
+ * returns once its entries are published.  The receiver is unchanged.  Lost
+ * senders: a lock held past the lock timeout TL is taken over (acquisition-
+ * counted lock word), a reservation stuck at the tail for TL becomes a PAD the
+ * receiver skips (its sender's commit then fails: RING_EDROPPED), and claims
+ * first publish committed entries left behind.  Not combinable with
+ * RING_CREATE_FAULT_TOLERANT. */
 #define RING_CREATE_RESERVE_COMMIT 4u
 
 /* Geometry limits (R5, R8) */
@@ -250,7 +254,10 @@ ring_status_t ring_stage_scale_bf16_put(ring_peer_t peer, const void* d_in, uint
  * The labelled sender actions of PAPER.md:778-789 at which a put can be made to
  * stop for good (a lost sender) or to pause (a delayed sender) while another
  * sender takes the lock over.  Applies to message `msg` of every later launch
- * of this attachment on a RING_CREATE_FAULT_TOLERANT ring. */
+ * of this attachment on a RING_CREATE_FAULT_TOLERANT ring.  On a
+ * RING_CREATE_RESERVE_COMMIT ring only die_after is used: RING_AT_LOCK = lost
+ * holding the lock right after its round's claims, RING_AT_WB = lost after the
+ * claims and the unlock, before any copy or commit (a hole). */
 #define RING_AT_LOCK 1u  /* after Lock (step 1) */
 #define RING_AT_GH 2u    /* after GH (steps 2-4: tail, head, stale-slot check) */
 #define RING_AT_WB 3u    /* after WB (step 5: header + payload written) */

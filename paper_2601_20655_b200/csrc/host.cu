@@ -577,7 +577,7 @@ ring_status_t ring_stage_scale_bf16_put(ring_peer_t p, const void* d_in, uint64_
 }
 
 ring_status_t ring_peer_set_fault(ring_peer_t p, const ring_fault_t* f) {
-  if (!p || !p->desc.ft) return RING_EINVAL;
+  if (!p || !(p->desc.ft || p->desc.rc)) return RING_EINVAL;
   if (!f) {
     p->fault = FaultSpec{};
     return RING_OK;
@@ -907,6 +907,7 @@ ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, 
   a.dests = r->dests_dev;
   a.dest0 = r->dests[0]->desc;
   a.n_dests = (uint32_t)r->dests.size();
+  a.lock_timeout_ns = g_lock_timeout_ns;
   a.routes = r->routes_dev;
   a.n_routes = r->max_routes;
   a.crc_table = r->crc;

@@ -61,6 +61,8 @@ struct LeaderState {
   uint32_t loaded;
   uint32_t items, units;
   bool aborted;
+  bool dead;                        // fault injection (reserve-then-commit): the sender is lost
+  uint64_t me;                      // reserve-then-commit: this round's lock word
 };
 
 __device__ __forceinline__ void write_pad_plan(LaunchCtx* ctx, uint32_t item, uint32_t dest, uint32_t slot,
@@ -82,6 +84,64 @@ struct MsgBrief {        // the fields lane 0 needs, computed in parallel by all
   uint32_t _p;
   uint64_t t_arr;        // arrival time (hdr.accepted_at): fast-reject admission
 };
+
+constexpr int kTagShift = 40;
+constexpr uint64_t kTagMask = (1ull << 22) - 1;
+constexpr uint64_t kFLow = (1ull << kTagShift) - 1;
+__device__ __forceinline__ uint64_t tagged_word(uint64_t w, uint32_t q) { return w | ((q & kTagMask) << kTagShift); }
+
+template <bool SYS>
+__device__ __forceinline__ uint64_t dcas(uint64_t* p, uint64_t cmp, uint64_t val) { return cas_acq_rel<SYS>(p, cmp, val); }
+__device__ __forceinline__ uint64_t dcas(const DestDesc& D, uint64_t* p, uint64_t cmp, uint64_t val) {
+  return D.sys ? dcas<true>(p, cmp, val) : dcas<false>(p, cmp, val);
+}
+__device__ __forceinline__ uint64_t dld(const DestDesc& D, const uint64_t* p) {
+  return D.sys ? ld_acquire<true>(p) : ld_acquire<false>(p);
+}
+
+// ---- reserve-then-commit helpers (oracle/reserve.py) -------------------------
+// Move the tail over the leading run of committed slots of [tail, resv)
+// (serial; the publisher has a warp-parallel version).  Returns the tail.
+__device__ uint64_t rc_help_advance(const DestDesc& D) {
+  uint64_t T = dld(D, tail_w(D));
+  while (true) {
+    const uint64_t Rv = dld(D, resv_w(D)), H = read_head(D);
+    const uint32_t tq = ptr_seq(T);
+    if (tq == ptr_seq(Rv) || seq_dist(tq, ptr_seq(H)) >= D.N) return T;
+    const uint64_t w = dld(D, slot_w(D, tq));
+    if (!(w & kBusy)) return T;
+    const uint64_t T2 = pack_ptr(advance(ptr_off(T), w & kFLow, D.R), seq_inc(tq));
+    const uint64_t old = dcas(D, tail_w(D), T, T2);
+    T = old == T ? T2 : old;
+  }
+}
+// A reservation stuck at the tail: after it has been observed unchanged for
+// TL its sender is presumed lost and the slot becomes a PAD (reserved ->
+// busy|pad, CAS) that the receiver skips.  `seen`/`since` carry the watch.
+__device__ void rc_hole_watch(const PutArgs& a, const DestDesc& D, uint64_t& seen, uint64_t& since) {
+  const uint64_t T = dld(D, tail_w(D));
+  const uint64_t w = dld(D, slot_w(D, ptr_seq(T)));
+  const uint64_t key = (w & kResvBit) ? (T ^ (w << 1)) | 1ull : 0ull;
+  const uint64_t now = globaltimer();
+  if (!key) { seen = 0; return; }
+  if (key != seen) { seen = key; since = now; return; }
+  if (now - since > a.lock_timeout_ns) {
+    dcas(D, slot_w(D, ptr_seq(T)), w, kBusy | kPad | (w & kFLow));
+    seen = 0;
+  }
+}
+// The ring lock with take-over of a lost holder (same word for TL).
+__device__ bool rc_lock(const PutArgs& a, const DestDesc& D, uint64_t me, uint64_t t_start) {
+  uint64_t seen = 0, seen_at = 0;
+  while (true) {
+    const uint64_t old = dcas(D, lock_w(D), 0ull, me);
+    if (old == 0) return true;
+    const uint64_t now = globaltimer();
+    if (old != seen) { seen = old; seen_at = now; }
+    else if (now - seen_at > a.lock_timeout_ns && dcas(D, lock_w(D), old, me) == old) return true;
+    if (now - t_start > a.timeout_ns) return false;
+  }
+}
 
 __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, LeaderState& L, uint32_t k0,
                                  uint32_t gmax, GroupSlot* gs, const MsgBrief* brief, const DestDesc* dests) {
@@ -145,7 +205,13 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
       // after our own previous items (and their Unlock) are published.
       while (!D.rc && ld_acquire_gpu32(&S->pub_seq) != L.items)   // RC: the leader unlocks itself
         if (globaltimer() - t_start > a.timeout_ns) { o.status = RING_ETIMEDOUT; break; }
-      if (o.status == RING_OK) {
+      if (o.status == RING_OK && D.rc) {
+        // reserve-then-commit: a lock word with an acquisition count, taken
+        // over from a lost holder after TL (the lock is held only for claims)
+        L.me = ((uint64_t)(++D.st->lock_acq) << 16) | (uint64_t)(D.producer_id + 1);
+        locked = rc_lock(a, D, L.me, t_start);
+        if (!locked) o.status = RING_ETIMEDOUT;
+      } else if (o.status == RING_OK) {
         const uint64_t me = (uint64_t)D.producer_id + 1;
         while (true) {
           const uint64_t old = D.sys ? cas_acquire<true>(lock_w(D), 0ull, me) : cas_acquire<false>(lock_w(D), 0ull, me);
@@ -154,9 +220,11 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         }
       }
       if (locked && D.rc) {
-        // reserve-then-commit: claim from the reservation frontier (entries
-        // between the tail and it are reserved or committed, not lost)
-        P = D.sys ? ld_relaxed<true>(resv_w(D)) : ld_relaxed<false>(resv_w(D));
+        // reserve-then-commit: first publish committed entries a sender left
+        // behind (as GH repairs Case 7), then claim from the reservation
+        // frontier (entries between the tail and it are reserved or committed)
+        rc_help_advance(D);
+        P = dld(D, resv_w(D));
         L.heads[d] = read_head(D);
         held = (int)d;
       } else if (locked) {
@@ -219,6 +287,32 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         const uint64_t H2 = read_head(D);
         if (H2 != H) { L.heads[d] = H2; continue; }
         if (a.flags & RING_TRY) { o.status = RING_FULL; break; }   // "release the lock and abort"
+        if (D.rc && l == 0) {
+          // reserve-then-commit: wait for credit WITHOUT the lock (it is only
+          // for claims; a holder waiting past TL would be taken over), helping
+          // to publish committed entries and turning a lost sender's
+          // reservation at the tail into a PAD; then claim again
+          st_release<false>(&S->planned, make_planned(L.items, L.units));   // our PADs to the publisher
+          dcas(D, lock_w(D), L.me, 0ull);
+          held = -1;
+          if (!t_start) t_start = globaltimer();
+          uint64_t seen = 0, since = 0;
+          bool moved = false;
+          while (!moved) {
+            if (globaltimer() - t_start > a.timeout_ns) break;
+            rc_help_advance(D);
+            rc_hole_watch(a, D, seen, since);
+            moved = read_head(D) != H2;
+          }
+          if (!moved) { o.status = RING_ETIMEDOUT; break; }
+          L.me = ((uint64_t)(++D.st->lock_acq) << 16) | (uint64_t)(D.producer_id + 1);
+          if (!rc_lock(a, D, L.me, t_start)) { o.status = RING_ETIMEDOUT; break; }
+          held = (int)d;
+          rc_help_advance(D);
+          P = dld(D, resv_w(D));
+          L.heads[d] = read_head(D);
+          continue;
+        }
         if (l > 0) {
           // Hand what is decided (and any PAD just planned) to the copy
           // warps and the publisher (and release the lock) before waiting.
@@ -259,11 +353,15 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
     gs[l] = o;
   }
   if (held >= 0 && dests[held].rc) {
-    // reserve-then-commit: the claims are done -- unlock now (release orders
-    // the reserved slots and the frontier before it); copies and commits
-    // happen outside the lock
+    // reserve-then-commit: the claims are done -- unlock now (acq_rel CAS:
+    // orders the reserved slots and the frontier before it; fails harmlessly
+    // if the lock was taken over); copies and commits happen outside the lock.
+    // Fault injection (tests): a sender lost holding the lock, or after its
+    // claims before any commit.
     const DestDesc& D = dests[held];
-    if (D.sys) st_release<true>(lock_w(D), 0ull); else st_release<false>(lock_w(D), 0ull);
+    const bool hit = a.fault.die_after && k0 <= a.fault.msg && a.fault.msg < k0 + done_l;
+    if (!(hit && a.fault.die_after == RING_AT_LOCK)) dcas(D, lock_w(D), L.me, 0ull);
+    if (hit) L.dead = true;
   } else if (held >= 0) {
     // Step 8 "Release the lock" after the round's LAST item (a PAD planned
     // for a deferred message comes after the last message item).
@@ -392,20 +490,6 @@ __device__ uint32_t fast_place(const PutArgs& a, LaunchCtx* ctx, LeaderState& L,
 // (one plan item per message; the publisher only counts it).  Tagged slot
 // words: busy | pad | (seq mod 2^22) << 40 | f (reading R21).
 // ---------------------------------------------------------------------------
-constexpr int kTagShift = 40;
-constexpr uint64_t kTagMask = (1ull << 22) - 1;
-constexpr uint64_t kFLow = (1ull << kTagShift) - 1;
-__device__ __forceinline__ uint64_t tagged_word(uint64_t w, uint32_t q) { return w | ((q & kTagMask) << kTagShift); }
-
-template <bool SYS>
-__device__ __forceinline__ uint64_t dcas(uint64_t* p, uint64_t cmp, uint64_t val) { return cas_acq_rel<SYS>(p, cmp, val); }
-__device__ __forceinline__ uint64_t dcas(const DestDesc& D, uint64_t* p, uint64_t cmp, uint64_t val) {
-  return D.sys ? dcas<true>(p, cmp, val) : dcas<false>(p, cmp, val);
-}
-__device__ __forceinline__ uint64_t dld(const DestDesc& D, const uint64_t* p) {
-  return D.sys ? ld_acquire<true>(p) : ld_acquire<false>(p);
-}
-
 // Fault injection point `at` for message k (lane 0).  Returns true if the
 // sender must stop for good here.
 __device__ bool ft_point(const PutArgs& a, uint32_t at, uint32_t k, uint64_t timeout_ns) {
@@ -613,6 +697,7 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     L.items = 0;
     L.units = 0;
     L.aborted = false;
+    L.dead = false;
   }
   __syncwarp();
   for (uint32_t k0 = 0; k0 < a.n;) {
@@ -657,9 +742,15 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     uint32_t g = 0;
     if (fast && !L.aborted) g = fast_place(a, ctx, L, gmax, gs, brief, a.dest0);
     if (g == 0) {
+      const uint32_t it0 = L.items, un0 = L.units;
       if (lane == 0) s_g = leader_place(a, ctx, S, L, k0, gmax, gs, brief, s_dests);
       __syncwarp();
       g = s_g;
+      if (L.dead) {              // fault injection: the sender is lost, this round is never planned
+        if (lane == 0) { L.items = it0; L.units = un0; }
+        __syncwarp();
+        break;
+      }
     }
     // placements: one release hands the round's copies (and headers) out
     const uint32_t k = k0 + lane;
@@ -707,7 +798,7 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   }
   if (lane == 0) {
     st_release<false>(&S->planned, make_planned(L.items, L.units) | kPlannedDone);
-    for (uint32_t d = 0; d < kMaxRouterDests && d < a.n_dests; ++d)
+    for (uint32_t d = 0; d < kMaxRouterDests && d < a.n_dests && !L.dead; ++d)
       if (L.loaded & (1u << d)) {
         a.dests[d].st->chan_seq = L.chans[d];
         if (!a.dests[d].mpsc) a.dests[d].st->tail_cache = L.tails[d];
@@ -862,8 +953,15 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
       // the leading run of committed slots -- ours or another sender's.
       if (pend) flush();
       if (D.sys) fence_acq_rel<true>(); else fence_acq_rel<false>();
-      if (mine && (flags & kEntry) && !(slot_word & kPad))
-        dcas(D, slot_w(D, slot), kResvBit | (slot_word & ((1ull << 40) - 1)), slot_word);
+      bool committed = false;
+      if (mine && (flags & kEntry) && !(slot_word & kPad)) {
+        const uint64_t want = kResvBit | (slot_word & ((1ull << 40) - 1));
+        committed = dcas(D, slot_w(D, slot), want, slot_word) == want;
+        if (!committed) a.status[ld_cg32(&ctx->plan[j % kPlanRing].msg)] = RING_EDROPPED;   // reservation taken (TL)
+      }
+      // wait until the tail has passed our last committed entry of the run
+      const uint32_t cm = __ballot_sync(0xffffffffu, committed);
+      const uint32_t last_seq = cm ? __shfl_sync(0xffffffffu, slot, 31 - __clz(cm)) : 0u;
       __syncwarp();
       {
         // warp-parallel: the lanes read up to 32 slots from the tail, the
@@ -874,6 +972,8 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
         T = __shfl_sync(0xffffffffu, T, 0);
         Rv = __shfl_sync(0xffffffffu, Rv, 0);
         H = __shfl_sync(0xffffffffu, H, 0);
+        uint64_t seen = 0, since = 0;
+        const uint64_t t0 = globaltimer();
         while (true) {
           const uint32_t tq = ptr_seq(T);
           const uint32_t room = D.N - min(D.N, seq_dist(tq, ptr_seq(H)));
@@ -882,7 +982,17 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
           if ((uint32_t)lane < k) w = dld(D, slot_w(D, (tq + lane) & kSeqMask));
           const uint32_t notbusy = __ballot_sync(0xffffffffu, !((uint32_t)lane < k && (w & kBusy)));
           const uint32_t nrun = notbusy ? __ffs(notbusy) - 1 : 32u;
-          if (nrun == 0) break;                             // the tail's slot is reserved, not committed yet
+          if (nrun == 0) {
+            // the tail's slot is reserved, not committed yet: done if our
+            // entries are published; else wait (a lost reservation becomes a PAD)
+            if (!cm || seq_dist(tq, last_seq) - 1u < (1u << 23) || globaltimer() - t0 > a.timeout_ns) break;
+            if (lane == 0) rc_hole_watch(a, D, seen, since);
+            if (lane == 0) { T = dld(D, tail_w(D)); Rv = dld(D, resv_w(D)); H = read_head(D); }
+            T = __shfl_sync(0xffffffffu, T, 0);
+            Rv = __shfl_sync(0xffffffffu, Rv, 0);
+            H = __shfl_sync(0xffffffffu, H, 0);
+            continue;
+          }
           const uint64_t fsum = warp_sum64((uint32_t)lane < nrun ? (w & ((1ull << 40) - 1)) : 0);
           const uint64_t T2 = pack_ptr((ptr_off(T) + fsum) % D.R, tq + nrun);
           uint64_t old = 0;

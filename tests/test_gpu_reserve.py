@@ -76,3 +76,53 @@ def test_reserve_commit_concurrent_producers(R, cross):
     for pe in peers:
         R.ring_detach(pe)
     R.ring_destroy(ring)
+
+
+@pytest.mark.parametrize("die_at", ["lock", "wb"])
+def test_reserve_commit_lost_sender(R, die_at):
+    """A sender lost with its reservation made -- holding the lock (RING_AT_LOCK)
+    or after unlocking, before its copy and commit (RING_AT_WB): the next sender
+    takes the lock over after TL, its entries wait behind the hole until, after
+    TL, the hole becomes a PAD the receiver skips (oracle/reserve.py crash
+    mode); the live sender's messages arrive complete, in order, at the places
+    the oracle's placement rule gives when the lost entry is kept as padding."""
+    R.ring_set_lock_timeout_ns(50_000)
+    L = Layout(1 << 16, 16)
+    ring = R.ring_create(0, L.R, L.N, 2, R.RING_CREATE_RESERVE_COMMIT | R.RING_CREATE_LOCAL)
+    h = R.ring_export(ring)
+    peers = []
+    for pid in range(2):
+        pe, mh = R.ring_attach_peer(h, 0, pid)
+        R.ring_bind_mirror(ring, pid, mh)
+        peers.append(pe)
+    xs = synth.random_stream(synth.SEED_BASE + 81, 0, 1, 100, 3000)
+    ys = synth.random_stream(synth.SEED_BASE + 81, 1, 3, 100, 3000)
+    keep = []
+    for pid, stream in ((0, xs), (1, ys)):
+        b, s = upload(stream, "cuda:0")
+        keep += [b, msg_tensor(stream, s, "cuda:0")]
+    arrived = torch.zeros(8, dtype=torch.int32).pin_memory()
+    go = torch.zeros(8, dtype=torch.int32).pin_memory()
+    R.ring_peer_set_fault(peers[0], R.RING_AT_LOCK if die_at == "lock" else R.RING_AT_WB, 0, 0, arrived, go)
+    stx = torch.full((1,), 10, dtype=torch.int32, device="cuda:0")
+    sty = torch.full((3,), 10, dtype=torch.int32, device="cuda:0")
+    R.ring_put_batch(peers[0], keep[1], 1, 0, stx)
+    torch.cuda.synchronize()
+    R.ring_put_batch(peers[1], keep[3], 3, 0, sty)
+    torch.cuda.synchronize()
+    assert stx.cpu().tolist() == [R.RING_EPENDING] and sty.cpu().tolist() == [0, 0, 0]
+    vt = torch.zeros(4 * 128, dtype=torch.uint8, device="cuda:0")
+    R.ring_consume(ring, 4, vt, None, 0, R.RING_TRY)
+    torch.cuda.synchronize()
+    v = views_host(vt)
+    assert [int(x["status"]) for x in v] == [0, 0, 0, R.RING_EMPTY]
+    hs = [decode_header(bytes(x["header"])) for x in v[:3]]
+    assert [(h["producer_id"], h["seq"]) for h in hs] == [(1, 0), (1, 1), (1, 2)]
+    img = [e for e in spsc_image(L, [xs[0].length] + [m.length for m in ys])["entries"] if not e[3]]
+    assert [(int(x["slot_seq"]), int(x["start"]), int(x["footprint"])) for x in v[:3]] == [tuple(e[:3]) for e in img[1:]]
+    for x, m in zip(v[:3], ys):
+        assert R.ring_read_data(ring, int(x["offset"]), int(x["len"])) == m.payload.tobytes()
+    R.ring_set_lock_timeout_ns(200_000)
+    for pe in peers:
+        R.ring_detach(pe)
+    R.ring_destroy(ring)
