@@ -82,8 +82,9 @@ typedef enum {
  * (reserved -> busy) and any sender moves the tail over the leading run of
  * committed slots (CAS), so entries are published in claim order; a put
  * returns once its entries are published.  The receiver is unchanged.  Lost
- * senders: a lock held past the lock timeout TL is taken over (acquisition-
- * counted lock word), a reservation stuck at the tail for TL becomes a PAD the
+ * senders: a lock held past the hole timeout is taken over (acquisition-
+ * counted lock word), a reservation stuck at the tail for the hole timeout
+ * (ring_set_hole_timeout_ns) becomes a PAD the
  * receiver skips (its sender's commit then fails: RING_EDROPPED), and claims
  * first publish committed entries left behind.  Not combinable with
  * RING_CREATE_FAULT_TOLERANT. */
@@ -273,8 +274,14 @@ typedef struct {
 } ring_fault_t;
 /* NULL clears.  RING_EINVAL unless the ring is fault tolerant. */
 ring_status_t ring_peer_set_fault(ring_peer_t peer, const ring_fault_t* fault);
-/* Lock timeout TL of fault-tolerant rings (default 200 us). */
+/* Lock timeout TL of fault-tolerant and reserve-then-commit rings (default 200 us). */
 ring_status_t ring_set_lock_timeout_ns(uint64_t ns);
+/* Reserve-then-commit rings: a reservation left uncommitted at the tail this
+ * long is a lost sender's and becomes a PAD, and a lock word unchanged this
+ * long is taken over (default 50 ms; must exceed the longest claim-to-commit
+ * time of a live sender, i.e. its largest copy, and a claim round under a
+ * saturated NVLink). */
+ring_status_t ring_set_hole_timeout_ns(uint64_t ns);
 
 /* ---- consumer ------------------------------------------------------------------
  * ring_get: receive the next `n` entries (receiver steps 1-3, PAPER.md:711-715,

@@ -130,7 +130,7 @@ class RCSim:
                     acts.append(("TL", pid))              # take over a lost sender's lock
                 continue
             if p.pc == "RH" and self.head == p.seen_head and not self._can_advance() and self._hole() is None:
-                continue                                  # (a committed entry or a hole at the tail also wakes it)
+                continue                                  # (a committed entry or a hole at the tail: it helps)
             if p.pc in ("Adv", "AdvW") and not self._can_advance():
                 if self._hole() is not None:
                     acts.append(("fill", pid))            # reservation of a lost sender -> PAD
@@ -196,18 +196,6 @@ class RCSim:
             p.pc = "Claim"
             return f"Lock({me})"
         if p.pc == "Claim":
-            q = self._hole()
-            if q is not None:                             # a lost sender's reservation at the tail -> PAD
-                w = self.slots[q % L.N]
-                self.slots[q % L.N] = BUSY | PADBIT | (w & F40)
-                return f"Fill({me})"
-            if self._can_advance():
-                # like GH's repair (Case 7): first publish committed entries a
-                # sender left unpublished (e.g. lost right after its commit)
-                t_b, t_q = unpack(self.tail)
-                w = self.slots[t_q % L.N]
-                self.tail = pack(adv(L, t_b, w & F40), seq_next(t_q))
-                return f"UH({me})"
             # steps 2-4 on the reservation frontier (space rule R4, PAD R3)
             p.p_b, p.p_q = unpack(self.resv)
             h_b, h_q = unpack(self.head)
@@ -243,6 +231,20 @@ class RCSim:
             p.pc = "WB" if p.pc == "Unlock" else "AdvW"
             return f"Unlock({me})"
         if p.pc == "RH":
+            # waiting for credit without the lock: help publish committed
+            # entries (e.g. of a sender lost right after its commit, as GH
+            # repairs Case 7) and turn a lost reservation into a PAD; claim
+            # again once the head has moved
+            q = self._hole()
+            if q is not None:
+                w = self.slots[q % L.N]
+                self.slots[q % L.N] = BUSY | PADBIT | (w & F40)
+                return f"Fill({me})"
+            if self._can_advance():
+                t_b, t_q = unpack(self.tail)
+                w = self.slots[t_q % L.N]
+                self.tail = pack(adv(L, t_b, w & F40), seq_next(t_q))
+                return f"UH({me})"
             p.pc = "Lock"
             return f"RH({me})"
         if p.pc == "WB":                                  # outside the lock

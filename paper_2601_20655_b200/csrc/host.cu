@@ -25,6 +25,7 @@ namespace {
 thread_local char g_cuda_err[512] = "";
 std::atomic<uint64_t> g_timeout_ns{2000000000ull};
 std::atomic<uint64_t> g_lock_timeout_ns{200000ull};   // TL of fault-tolerant rings
+std::atomic<uint64_t> g_hole_timeout_ns{50000000ull}; // reserve-then-commit hole timeout (50 ms)
 std::atomic<uint64_t> g_launches{0};
 std::mutex g_mu;
 const uint32_t g_token = 0x9e3779b9u ^ (uint32_t)getpid() ^ (uint32_t)((uintptr_t)&g_mu & 0xffffffffu);
@@ -215,6 +216,11 @@ const char* ring_strerror(ring_status_t s) {
   return "unknown";
 }
 const char* ring_last_cuda_error(void) { return g_cuda_err; }
+ring_status_t ring_set_hole_timeout_ns(uint64_t ns) {
+  if (ns == 0) return RING_EINVAL;
+  g_hole_timeout_ns = ns;
+  return RING_OK;
+}
 ring_status_t ring_set_lock_timeout_ns(uint64_t ns) {
   if (ns == 0) return RING_EINVAL;
   g_lock_timeout_ns = ns;
@@ -642,6 +648,7 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   a.dest0 = p->desc;
   a.n_dests = 1;
   a.lock_timeout_ns = g_lock_timeout_ns;
+  a.hole_timeout_ns = g_hole_timeout_ns;
   a.fault = p->fault;
   a.crc_table = p->crc;
   a.timeout_ns = g_timeout_ns;
@@ -908,6 +915,7 @@ ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, 
   a.dest0 = r->dests[0]->desc;
   a.n_dests = (uint32_t)r->dests.size();
   a.lock_timeout_ns = g_lock_timeout_ns;
+  a.hole_timeout_ns = g_hole_timeout_ns;
   a.routes = r->routes_dev;
   a.n_routes = r->max_routes;
   a.crc_table = r->crc;

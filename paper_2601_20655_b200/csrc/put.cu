@@ -116,7 +116,8 @@ __device__ uint64_t rc_help_advance(const DestDesc& D) {
   }
 }
 // A reservation stuck at the tail: after it has been observed unchanged for
-// TL its sender is presumed lost and the slot becomes a PAD (reserved ->
+// the hole timeout (longer than any live sender's claim-to-commit time: a
+// copy of the largest message) its sender is presumed lost and the slot becomes a PAD (reserved ->
 // busy|pad, CAS) that the receiver skips.  `seen`/`since` carry the watch.
 __device__ void rc_hole_watch(const PutArgs& a, const DestDesc& D, uint64_t& seen, uint64_t& since) {
   const uint64_t T = dld(D, tail_w(D));
@@ -125,12 +126,15 @@ __device__ void rc_hole_watch(const PutArgs& a, const DestDesc& D, uint64_t& see
   const uint64_t now = globaltimer();
   if (!key) { seen = 0; return; }
   if (key != seen) { seen = key; since = now; return; }
-  if (now - since > a.lock_timeout_ns) {
+  if (now - since > a.hole_timeout_ns) {
     dcas(D, slot_w(D, ptr_seq(T)), w, kBusy | kPad | (w & kFLow));
+    if (a.trace) atomicAdd(reinterpret_cast<unsigned long long*>(a.trace + 1891), 1ull);
     seen = 0;
   }
 }
-// The ring lock with take-over of a lost holder (same word for TL).
+// The ring lock with take-over of a lost holder (same word for the hole
+// timeout: a live holder's claims can take tens of microseconds when NVLink
+// is saturated by copies, so the short TL would take over live holders).
 __device__ bool rc_lock(const PutArgs& a, const DestDesc& D, uint64_t me, uint64_t t_start) {
   uint64_t seen = 0, seen_at = 0;
   while (true) {
@@ -138,7 +142,10 @@ __device__ bool rc_lock(const PutArgs& a, const DestDesc& D, uint64_t me, uint64
     if (old == 0) return true;
     const uint64_t now = globaltimer();
     if (old != seen) { seen = old; seen_at = now; }
-    else if (now - seen_at > a.lock_timeout_ns && dcas(D, lock_w(D), old, me) == old) return true;
+    else if (now - seen_at > a.hole_timeout_ns && dcas(D, lock_w(D), old, me) == old) {
+      if (a.trace) atomicAdd(reinterpret_cast<unsigned long long*>(a.trace + 1890), 1ull);
+      return true;
+    }
     if (now - t_start > a.timeout_ns) return false;
   }
 }
@@ -220,10 +227,11 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         }
       }
       if (locked && D.rc) {
-        // reserve-then-commit: first publish committed entries a sender left
-        // behind (as GH repairs Case 7), then claim from the reservation
-        // frontier (entries between the tail and it are reserved or committed)
-        rc_help_advance(D);
+        // reserve-then-commit: claim from the reservation frontier (entries
+        // between the tail and it are reserved or committed).  Nothing slow
+        // under the lock: a holder past TL would be taken over (publishing
+        // committed entries left behind is done without it, below and by the
+        // publishers)
         P = dld(D, resv_w(D));
         L.heads[d] = read_head(D);
         held = (int)d;
@@ -308,7 +316,6 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
           L.me = ((uint64_t)(++D.st->lock_acq) << 16) | (uint64_t)(D.producer_id + 1);
           if (!rc_lock(a, D, L.me, t_start)) { o.status = RING_ETIMEDOUT; break; }
           held = (int)d;
-          rc_help_advance(D);
           P = dld(D, resv_w(D));
           L.heads[d] = read_head(D);
           continue;
@@ -850,6 +857,48 @@ __device__ __forceinline__ void write_header(const PutArgs& a, LaunchCtx* ctx, u
   }
 }
 
+// Reserve-then-commit: move the tail over the leading run of committed slots,
+// warp-parallel (the lanes read up to 32 slots from the tail; entries tile the
+// ring and PADs fill every wrap, so offsets add mod R; ONE CAS per run).  With
+// `wait`, keep going until the tail has passed seq `last` (our last committed
+// entry), turning a reservation stuck at the tail for the hole timeout into a
+// PAD (a lost sender, reading R23).
+__device__ void rc_advance(const PutArgs& a, const DestDesc& D, int lane, bool wait, uint32_t last) {
+  uint64_t T = 0, Rv = 0, H = 0;
+  if (lane == 0) { T = dld(D, tail_w(D)); Rv = dld(D, resv_w(D)); H = read_head(D); }
+  T = __shfl_sync(0xffffffffu, T, 0);
+  Rv = __shfl_sync(0xffffffffu, Rv, 0);
+  H = __shfl_sync(0xffffffffu, H, 0);
+  uint64_t seen = 0, since = 0;
+  const uint64_t t0 = globaltimer();
+  while (true) {
+    const uint32_t tq = ptr_seq(T);
+    const uint32_t room = D.N - min(D.N, seq_dist(tq, ptr_seq(H)));
+    const uint32_t k = min(min(seq_dist(ptr_seq(Rv), tq), room), 32u);
+    uint64_t w = 0;
+    if ((uint32_t)lane < k) w = dld(D, slot_w(D, (tq + lane) & kSeqMask));
+    const uint32_t notbusy = __ballot_sync(0xffffffffu, !((uint32_t)lane < k && (w & kBusy)));
+    const uint32_t nrun = notbusy ? __ffs(notbusy) - 1 : 32u;
+    if (nrun == 0) {
+      if (!wait || seq_dist(tq, last) - 1u < (1u << 23) || globaltimer() - t0 > a.timeout_ns) return;
+      if (lane == 0) {
+        rc_hole_watch(a, D, seen, since);
+        T = dld(D, tail_w(D)); Rv = dld(D, resv_w(D)); H = read_head(D);
+      }
+      T = __shfl_sync(0xffffffffu, T, 0);
+      Rv = __shfl_sync(0xffffffffu, Rv, 0);
+      H = __shfl_sync(0xffffffffu, H, 0);
+      continue;
+    }
+    const uint64_t fsum = warp_sum64((uint32_t)lane < nrun ? (w & kFLow) : 0);
+    const uint64_t T2 = pack_ptr((ptr_off(T) + fsum) % D.R, tq + nrun);
+    uint64_t old = 0;
+    if (lane == 0) old = dcas(D, tail_w(D), T, T2);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    T = old == T ? T2 : old;                           // moved (look further) or somebody else did
+  }
+}
+
 // Steps 5-8 (WB header, WL, UH, Unlock), in item order.  As soon as items are
 // planned the lanes write their headers (write_header), off the copy critical
 // path.  For publication lane l caches the plan of item i + l (read once);
@@ -872,6 +921,8 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
   bool pend = false, pend_entries = false, pend_unlock = false;
   uint32_t pend_dest = 0, pend_n = 0;
   uint64_t pend_tail = 0;
+  bool rc_any = false;       // reserve-then-commit: committed entries to see published
+  uint32_t rc_last = 0, rc_dest = 0;
   if (a.trace && lane == 0) a.trace[255] = globaltimer();
   auto flush = [&]() {
     const DestDesc& D = a.dests[pend_dest];
@@ -957,49 +1008,20 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
       if (mine && (flags & kEntry) && !(slot_word & kPad)) {
         const uint64_t want = kResvBit | (slot_word & ((1ull << 40) - 1));
         committed = dcas(D, slot_w(D, slot), want, slot_word) == want;
-        if (!committed) a.status[ld_cg32(&ctx->plan[j % kPlanRing].msg)] = RING_EDROPPED;   // reservation taken (TL)
+        if (!committed) {
+          a.status[ld_cg32(&ctx->plan[j % kPlanRing].msg)] = RING_EDROPPED;   // reservation taken (TL)
+          if (a.trace) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.trace + 1892), 1ull);
+            a.trace[1893] = dld(D, slot_w(D, slot));
+            a.trace[1894] = want;
+          }
+        }
       }
-      // wait until the tail has passed our last committed entry of the run
       const uint32_t cm = __ballot_sync(0xffffffffu, committed);
-      const uint32_t last_seq = cm ? __shfl_sync(0xffffffffu, slot, 31 - __clz(cm)) : 0u;
+      if (cm) { rc_any = true; rc_last = __shfl_sync(0xffffffffu, slot, 31 - __clz(cm)); rc_dest = dest0; }
       __syncwarp();
       {
-        // warp-parallel: the lanes read up to 32 slots from the tail, the
-        // leading run of committed ones (entries tile the ring, PADs fill
-        // every wrap: offsets add mod R) moves the tail with ONE CAS
-        uint64_t T = 0, Rv = 0, H = 0;
-        if (lane == 0) { T = dld(D, tail_w(D)); Rv = dld(D, resv_w(D)); H = read_head(D); }
-        T = __shfl_sync(0xffffffffu, T, 0);
-        Rv = __shfl_sync(0xffffffffu, Rv, 0);
-        H = __shfl_sync(0xffffffffu, H, 0);
-        uint64_t seen = 0, since = 0;
-        const uint64_t t0 = globaltimer();
-        while (true) {
-          const uint32_t tq = ptr_seq(T);
-          const uint32_t room = D.N - min(D.N, seq_dist(tq, ptr_seq(H)));
-          const uint32_t k = min(min(seq_dist(ptr_seq(Rv), tq), room), 32u);
-          uint64_t w = 0;
-          if ((uint32_t)lane < k) w = dld(D, slot_w(D, (tq + lane) & kSeqMask));
-          const uint32_t notbusy = __ballot_sync(0xffffffffu, !((uint32_t)lane < k && (w & kBusy)));
-          const uint32_t nrun = notbusy ? __ffs(notbusy) - 1 : 32u;
-          if (nrun == 0) {
-            // the tail's slot is reserved, not committed yet: done if our
-            // entries are published; else wait (a lost reservation becomes a PAD)
-            if (!cm || seq_dist(tq, last_seq) - 1u < (1u << 23) || globaltimer() - t0 > a.timeout_ns) break;
-            if (lane == 0) rc_hole_watch(a, D, seen, since);
-            if (lane == 0) { T = dld(D, tail_w(D)); Rv = dld(D, resv_w(D)); H = read_head(D); }
-            T = __shfl_sync(0xffffffffu, T, 0);
-            Rv = __shfl_sync(0xffffffffu, Rv, 0);
-            H = __shfl_sync(0xffffffffu, H, 0);
-            continue;
-          }
-          const uint64_t fsum = warp_sum64((uint32_t)lane < nrun ? (w & ((1ull << 40) - 1)) : 0);
-          const uint64_t T2 = pack_ptr((ptr_off(T) + fsum) % D.R, tq + nrun);
-          uint64_t old = 0;
-          if (lane == 0) old = dcas(D, tail_w(D), T, T2);
-          old = __shfl_sync(0xffffffffu, old, 0);
-          T = old == T ? T2 : old;                           // moved (look further) or somebody else did
-        }
+        rc_advance(a, D, lane, false, 0u);
         if (lane == 0) st_u32_relaxed_gpu(&S->pub_seq, i + run);
       }
       i += run;
@@ -1043,6 +1065,10 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
     if (!full || unlock_now || run < 32 || pend_n >= 96) flush();
   }
   if (pend) flush();
+  // reserve-then-commit: the put returns once its entries are published --
+  // waited for only here, after every commit of the launch (waiting per run
+  // would hold back our later commits that other senders' entries wait on)
+  if (rc_any) rc_advance(a, a.dests[rc_dest], lane, true, rc_last);
 }
 
 // One warp per CTA: the first kSpecRounds rounds' placement as the leader will

@@ -177,7 +177,8 @@ struct PutArgs {
   uint32_t chunk;             // bytes per copy work unit
   uint32_t copy_mode;         // 0: LSU copy warps, 1: TMA engine per CTA
   uint32_t _pad;
-  uint64_t lock_timeout_ns;   // TL (fault-tolerant rings)
+  uint64_t lock_timeout_ns;   // TL (fault-tolerant and reserve-then-commit rings)
+  uint64_t hole_timeout_ns;   // reserve-then-commit: a reservation this old at the tail is a lost sender's
   FaultSpec fault;            // test-only fault injection
 };
 

@@ -103,6 +103,7 @@ def _load():
         "ring_peer_trace": [P, P, U32],
         "ring_peer_set_fault": [P, C.POINTER(ring_fault_t)],
         "ring_set_lock_timeout_ns": [U64],
+        "ring_set_hole_timeout_ns": [U64],
         "router_set_admission": [P, U32, C.c_uint16, U64, U32, P],
         "ring_peer_device_view": [P, C.POINTER(ring_dev_peer_t)],
         "ring_set_create": [C.POINTER(P), U32, C.POINTER(P)],
@@ -397,3 +398,7 @@ def ring_set_destroy(s: int) -> None:
 
 def ring_set_consume(s: int, n: int, d_views, d_ring_idx=None, flags: int = 0, stream=None) -> None:
     _check("ring_set_consume", lib.ring_set_consume(s, n, _ptr(d_views), _ptr(d_ring_idx), flags, _stream(stream)))
+
+
+def ring_set_hole_timeout_ns(ns: int) -> None:
+    _check("ring_set_hole_timeout_ns", lib.ring_set_hole_timeout_ns(int(ns)))

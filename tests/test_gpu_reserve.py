@@ -82,11 +82,11 @@ def test_reserve_commit_concurrent_producers(R, cross):
 def test_reserve_commit_lost_sender(R, die_at):
     """A sender lost with its reservation made -- holding the lock (RING_AT_LOCK)
     or after unlocking, before its copy and commit (RING_AT_WB): the next sender
-    takes the lock over after TL, its entries wait behind the hole until, after
-    TL, the hole becomes a PAD the receiver skips (oracle/reserve.py crash
+    takes the lock over, its entries wait behind the hole until the hole
+    becomes a PAD the receiver skips (both after the hole timeout) (oracle/reserve.py crash
     mode); the live sender's messages arrive complete, in order, at the places
     the oracle's placement rule gives when the lost entry is kept as padding."""
-    R.ring_set_lock_timeout_ns(50_000)
+    R.ring_set_hole_timeout_ns(1_000_000)
     L = Layout(1 << 16, 16)
     ring = R.ring_create(0, L.R, L.N, 2, R.RING_CREATE_RESERVE_COMMIT | R.RING_CREATE_LOCAL)
     h = R.ring_export(ring)
@@ -122,7 +122,7 @@ def test_reserve_commit_lost_sender(R, die_at):
     assert [(int(x["slot_seq"]), int(x["start"]), int(x["footprint"])) for x in v[:3]] == [tuple(e[:3]) for e in img[1:]]
     for x, m in zip(v[:3], ys):
         assert R.ring_read_data(ring, int(x["offset"]), int(x["len"])) == m.payload.tobytes()
-    R.ring_set_lock_timeout_ns(200_000)
+    R.ring_set_hole_timeout_ns(50_000_000)
     for pe in peers:
         R.ring_detach(pe)
     R.ring_destroy(ring)
