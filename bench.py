@@ -321,6 +321,33 @@ def bench_c2(args):
     torch.cuda.synchronize()
     e2e = m * plen * e_steps / (e0.elapsed_time(e1) / 1e3) / 1e9
 
+    # secondary line: copy-out consume (the consumer copies every payload out of
+    # the ring before releasing it: 4 bytes of HBM traffic per payload byte)
+    dst = torch.empty(m * plen, dtype=torch.uint8, device="cuda")
+    co_steps = max(4, min(args.steps, 400))
+    for i in range(3):
+        R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
+        R.ring_consume(ring, m, views, dst, plen, 0, sc)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(main)
+    sp.wait_stream(main)
+    sc.wait_stream(main)
+    for i in range(co_steps):
+        R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
+        R.ring_consume(ring, m, views, dst, plen, 0, sc)
+    main.wait_stream(sp)
+    main.wait_stream(sc)
+    c1.record(main)
+    torch.cuda.synchronize()
+    co_ms = c0.elapsed_time(c1)
+    co_ok = bool((status == 0).all().item()) and bool((R.parse_views(views.cpu().numpy())["status"] == 0).all())
+    copy_out = {"value": round(m * plen * co_steps / (co_ms / 1e3) / 1e9, 2), "unit": UNIT,
+                "ms_per_step": round(co_ms / co_steps, 5), "steps": co_steps, "ok": co_ok,
+                "roofline_payload_gbs": round(peaks["hbm_gbs"] / 4, 1),
+                "what": "same stream with ring_consume copying each payload out (copy-out mode, SURVEY.md d-3)"}
+    del dst
+
     cpu = cpu_baseline([plen] * 16, Rb, N, args.cpu_budget)
     R.ring_detach(peer)
     R.ring_destroy(ring)
@@ -334,7 +361,7 @@ def bench_c2(args):
                    "l2": "inputs larger than L2 (4 x 64 MiB rotating source sets + 64 MiB ring)",
                    "consume_mode": "view (zero copy)", "parallelism": "replicas only (1 ring)",
                    "streams": "put on one stream, consume on another; consume(s) overlaps put(s), "
-                              "put(s+1) waits for consume(s) (event)"},
+                              "put(s+1) takes credit as consume(s) releases entries (device-side waits)"},
         "msgs_per_s": round(m * args.steps / (ms / 1e3), 1),
         "latency_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99),
                        "what": "t_visible - t_put of the last step's 64 messages (same GPU clock; batched put, "
@@ -347,6 +374,7 @@ def bench_c2(args):
                      "algorithmic_bytes_per_launch": put_bytes},
         "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": m * stride,
                 "d2h_bytes_per_step": m * 128},
+        "copy_out": copy_out,
         "gpu_launches": int(launches),
         "clocks": clocks,
         "cpu_baseline": cpu,

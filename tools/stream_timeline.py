@@ -26,12 +26,13 @@ for s in range(4):
     d_msgs.append(torch.from_numpy(a.view(np.uint8).copy()).cuda())
 status = torch.zeros(m, dtype=torch.int32, device="cuda")
 views = torch.zeros(m * 128, dtype=torch.uint8, device="cuda")
+dst = torch.empty(m * plen, dtype=torch.uint8, device="cuda") if os.environ.get("COPYOUT") else None
 sp = torch.cuda.Stream()
 sc = torch.cuda.Stream(priority=-1) if os.environ.get("PRIO") else torch.cuda.Stream()
 steps = int(os.environ.get("STEPS", "12"))
 for i in range(6):
     R.ring_put_batch(peer, d_msgs[i % 4], m, 0, status, sp)
-    R.ring_consume(ring, m, views, None, 0, 0, sc)
+    R.ring_consume(ring, m, views, dst, plen if dst is not None else 0, 0, sc)
 torch.cuda.synchronize()
 ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
 with torch.cuda.stream(sp):
@@ -41,7 +42,7 @@ for i in range(steps):
     R.ring_put_batch(peer, d_msgs[i % 4], m, 0, status, sp)
     ev[i][1].record(sp)
     ev[i][2].record(sc)
-    R.ring_consume(ring, m, views, None, 0, 0, sc)
+    R.ring_consume(ring, m, views, dst, plen if dst is not None else 0, 0, sc)
     ev[i][3].record(sc)
 torch.cuda.synchronize()
 z = ev[0][0]
