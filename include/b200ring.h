@@ -304,7 +304,10 @@ ring_status_t ring_release(ring_t ring, uint32_t count, void* stream);
  * read (and copied, if d_dst != NULL): the paper's receiver loop as one launch. */
 ring_status_t ring_consume(ring_t ring, uint32_t n, ring_view_t* d_views, void* d_dst, uint64_t dst_stride,
                            uint32_t flags, void* stream);
-/* Tuning: CTAs / threads of the copy-out get (0 = default). */
+/* Tuning: CTAs / threads of the copy-out get (0 = default).  A copy-out get
+ * and a put on the SAME GPU spin on each other: one CTA of each must fit on an
+ * SM together (the defaults do: ~23 K + ~27 K registers); a get grid of 512
+ * threads per CTA does not, and the pair then only ends by timing out. */
 ring_status_t ring_config(ring_t ring, uint32_t copy_ctas, uint32_t threads);
 
 /* ---- inspection (tests, debugging; synchronous) ---------------------------------

@@ -289,7 +289,11 @@ __global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
   const int warp = threadIdx.x >> 5;
   __shared__ uint32_t s_crc[kCrcTableWords];
   __shared__ CopyShared cs;
-  if (threadIdx.x == 0) { cs.pl = 0; cs.owner = 0; }
+  if (threadIdx.x == 0) {
+    cs.pl = 0;
+    cs.owner = 0;
+    if (a.dst) cs.first = atomicAdd(&S->next_unit, (blockDim.x >> 5) - (blockIdx.x == 0 ? 2u : 0u));
+  }
   if (blockIdx.x == 0) {
     load_crc_table(s_crc, a.crc_table);   // (its __syncthreads also covers cs)
     if (warp == 0) {

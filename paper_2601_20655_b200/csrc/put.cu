@@ -1134,7 +1134,13 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
   __shared__ uint32_t s_crc[kCrcTableWords];
   __shared__ CopyShared cs;
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) { cs.pl = 0; cs.owner = 0; }
+  if (threadIdx.x == 0) {
+    cs.pl = 0;
+    cs.owner = 0;
+    // the block of first units of this CTA's copy warps (copy_mode 0)
+    const uint32_t ncw = (blockDim.x >> 5) - (blockIdx.x == 0 ? 2u : 0u);
+    if (MODE == 0) cs.first = atomicAdd(&S->next_unit, ncw);
+  }
   __syncthreads();
   if (blockIdx.x == 0) {
     if (a.trace && threadIdx.x == 0) a.trace[252] = globaltimer();

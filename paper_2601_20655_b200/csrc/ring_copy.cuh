@@ -112,12 +112,12 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
                                           const SpecRound* spec = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t cur = 0;   // items before `cur` hold no unit this warp can still take
-  // First unit: the warp's index among the grid's copy warps (CTA 0 keeps two
-  // control warps), no atomic -- ~1,000 warps taking their first unit with an
-  // atomicAdd on one word serialise for microseconds.  Later units: dynamic.
-  const uint32_t wpc = blockDim.x >> 5;
-  const uint32_t n_static = gridDim.x * wpc - 2;
-  uint32_t first = blockIdx.x == 0 ? (threadIdx.x >> 5) - 2 : (wpc - 2) + (blockIdx.x - 1) * wpc + (threadIdx.x >> 5);
+  // First unit: the CTA took a block of units for all its copy warps with ONE
+  // atomicAdd when it started (~1,000 warps each taking their first unit with
+  // an atomicAdd on one word serialise for microseconds); only a running CTA
+  // takes units, so a launch still never needs all its CTAs resident.  Later
+  // units: one atomicAdd each.
+  uint32_t first = cs->first + (threadIdx.x >> 5) - (blockIdx.x == 0 ? 2u : 0u);
   bool have_first = true;
   // debug timeline: the first unit of the first copy warp of each CTA
   uint64_t* tr = (trace && (threadIdx.x >> 5) == (blockIdx.x == 0 ? 2 : 0)) ? trace + 1280 + 4 * blockIdx.x : nullptr;
@@ -125,7 +125,7 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
     uint32_t u = 0, quit = 0, ps = 0;
     if (lane == 0) {
       if (tr) tr[0] = globaltimer();
-      u = have_first ? first : n_static + atomicAdd(&S->next_unit, 1u);
+      u = have_first ? first : atomicAdd(&S->next_unit, 1u);
       if (!(spec && u < spec->n_units)) {      // not covered by the CTA's speculative first round
         bool to = false;
         const uint64_t pl = wait_planned(S, cs, u, timeout_ns, to);
@@ -272,17 +272,16 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
   uint32_t pending_u = 0xffffffffu;         // unit taken but not planned yet
   bool exhausted = false;
   uint64_t wait_end = 0;
-  // the first STAGES units of every engine are static (strided over the grid:
-  // no atomic, low units first), later ones dynamic
-  uint32_t n_taken = 0;
-  const uint32_t n_static = (uint32_t)STAGES * gridDim.x;
+  // the engine's first STAGES units come from one atomicAdd, later ones one each
+  uint32_t n_taken = 0, first = 0;
+  if (lane == 0) first = atomicAdd(&S->next_unit, (uint32_t)STAGES);
   while (true) {
     // ---- refill free stages with planned units
     while (!exhausted && k_issue - k_done < (uint32_t)STAGES) {
       uint32_t u = 0, state = 0, ps = 0;    // state 0 = planned, 1 = not yet, 2 = exhausted
       if (lane == 0) {
         if (pending_u == 0xffffffffu)
-          pending_u = n_taken < (uint32_t)STAGES ? blockIdx.x + n_taken * gridDim.x : n_static + atomicAdd(&S->next_unit, 1u);
+          pending_u = n_taken < (uint32_t)STAGES ? first + n_taken : atomicAdd(&S->next_unit, 1u);
         u = pending_u;
         if (!(spec && u < spec->n_units)) {
           const uint64_t pl = ld_acquire<false>(&S->planned);

@@ -107,7 +107,7 @@ struct SpecRound {
 struct CopyShared {
   uint64_t pl;
   uint32_t owner;
-  uint32_t _p;
+  uint32_t first;       // first unit of the CTA's copy warps (one atomicAdd per CTA, taken at CTA start)
 };
 
 // Per-launch counters.  A context holds two sets used by alternate launches;

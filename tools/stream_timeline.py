@@ -17,6 +17,9 @@ ring = R.ring_create(0, Rb, N, 1, R.RING_CREATE_LOCAL)
 peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
 R.ring_bind_mirror(ring, 0, mh)
 R.ring_peer_config(peer, 148, int(os.environ.get("THREADS", "256")), 0)
+if os.environ.get("GET_CFG"):
+    gc, gt = (int(x) for x in os.environ["GET_CFG"].split(":"))
+    R.ring_config(ring, gc, gt)
 stride = 1 << 20
 src = torch.randint(0, 255, (4 * m * stride,), dtype=torch.uint8, device="cuda")
 d_msgs = []
