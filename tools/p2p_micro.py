@@ -7,7 +7,7 @@ import numpy as np, torch
 from paper_2601_20655_b200 import ring as R
 
 R.ring_set_timeout_ns(3_000_000_000)
-ring = R.ring_create(1, 64 << 20, 64, 1, 0)
+ring = R.ring_create(1, int(os.environ.get("RB", str(64 << 20))), int(os.environ.get("N", "64")), 1, 0)
 peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
 R.ring_bind_mirror(ring, 0, mh)
 src = torch.randint(0, 255, (160 << 20,), dtype=torch.uint8, device="cuda:0")
