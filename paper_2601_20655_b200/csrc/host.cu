@@ -658,7 +658,8 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   DevGuard g(p->device);
   default_grid(p->device, p->desc.sys, &ctas, &thr, &chunk);
   a.copy_mode = p->copy_mode;
-  if (a.copy_mode == 1 && chunk > (48u << 10)) chunk = 48u << 10;   // engine stages live in shared memory
+  // engine stages live in shared memory: the largest power of two that fits
+  while (a.copy_mode == 1 && chunk > 4096 && (uint64_t)chunk * kEngineStages > kEngineSmem) chunk >>= 1;
   a.chunk = chunk;
   a.launch = p->launches;
   if (getenv("B200RING_TRACE")) {

@@ -1185,7 +1185,7 @@ cudaError_t preload_put() {
   cudaError_t e = cudaFuncGetAttributes(&fa, put_kernel<0>);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, put_kernel<1>);
   if (e == cudaSuccess)   // TMA engine stages (up to kEngineStages x 48 KiB)
-    e = cudaFuncSetAttribute(put_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEngineStages * (48 << 10));
+    e = cudaFuncSetAttribute(put_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEngineSmem);
   return e;
 }
 

@@ -255,30 +255,68 @@ __device__ __forceinline__ void spec_lookup(const SpecRound* spec, uint32_t u, i
   }
 }
 
+template <int N>
+__device__ __forceinline__ void bulk_wait_group(uint32_t allow) {   // all but the `allow` newest groups complete
+  switch (allow) {
+    case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group 7;" ::: "memory"); break;
+  }
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read(uint32_t allow) {   // their smem reads done
+  switch (allow) {
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group.read 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory"); break;
+  }
+}
+
+// Pipelined TMA engine.  Counters over the engine's units in issue order:
+//   k_issue  loads issued (global -> shared, mbarrier complete_tx)
+//   k_store  stores issued (shared -> global, one bulk group each)
+//   k_free   stores whose shared-memory reads are done: the stage is reusable
+//   k_done   stores complete (global writes done): the unit is counted (arrive)
+// The next unit's control (take, planned check, find) is resolved while the
+// previous ones are in flight; stages are reused as soon as their store has
+// READ shared memory; arrives follow full completion, lazily (at most STAGES
+// stores outstanding).
 template <int STAGES>
 __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns, uint8_t* bufs,
                             const SpecRound* spec = nullptr) {
   const int lane = threadIdx.x & 31;
   __shared__ __align__(8) uint64_t bar[STAGES];
   __shared__ EngineStage st[STAGES];
+  __shared__ uint32_t items[2 * STAGES];    // item of unit k (k_issue - k_done <= 2 STAGES)
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  uint32_t phase = 0;                       // parity bit per stage (lane 0)
-  uint32_t k_issue = 0, k_store = 0, k_done = 0, cur = 0;
-  uint32_t pending_u = 0xffffffffu;         // unit taken but not planned yet
+  uint32_t phase = 0;                       // parity bit per stage
+  uint32_t k_issue = 0, k_store = 0, k_free = 0, k_done = 0, cur = 0;
+  uint32_t pending_u = 0xffffffffu;         // unit taken, not resolved yet
   bool exhausted = false;
   uint64_t wait_end = 0;
-  // the engine's first STAGES units come from one atomicAdd, later ones one each
-  uint32_t n_taken = 0, first = 0;
+  uint32_t n_taken = 0, first = 0;          // the first STAGES units come from one atomicAdd
   if (lane == 0) first = atomicAdd(&S->next_unit, (uint32_t)STAGES);
+  first = __shfl_sync(0xffffffffu, first, 0);
   while (true) {
-    // ---- refill free stages with planned units
-    while (!exhausted && k_issue - k_done < (uint32_t)STAGES) {
-      uint32_t u = 0, state = 0, ps = 0;    // state 0 = planned, 1 = not yet, 2 = exhausted
+    bool progress = false;
+    // ---- 1. resolve the next unit and load it into a free stage
+    if (!exhausted && k_issue - k_free < (uint32_t)STAGES) {
+      uint32_t u = 0, state = 0, ps = 0;    // 0 = planned, 1 = not yet, 2 = none left
       if (lane == 0) {
         if (pending_u == 0xffffffffu)
           pending_u = n_taken < (uint32_t)STAGES ? first + n_taken : atomicAdd(&S->next_unit, 1u);
@@ -289,102 +327,104 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
           else ps = planned_items(pl);
         }
       }
-      __syncwarp();
       state = __shfl_sync(0xffffffffu, state, 0);
-      if (state == 2) { exhausted = true; break; }
-      if (state == 1) {
-        if (k_done < k_issue) break;        // finish in-flight work first, never spin with it pending
-        const uint64_t t = globaltimer();
-        if (!wait_end) wait_end = t + 2 * timeout_ns;
-        else if (t > wait_end) { exhausted = true; break; }
-        __nanosleep(64);
-        continue;
+      if (state == 2) {
+        exhausted = true;
+      } else if (state == 1) {
+        if (k_done == k_issue) {            // nothing in flight: wait politely (bounded)
+          const uint64_t t = globaltimer();
+          if (!wait_end) wait_end = t + 2 * timeout_ns;
+          else if (t > wait_end) exhausted = true;
+          __nanosleep(64);
+        }
+      } else {
+        wait_end = 0;
+        u = __shfl_sync(0xffffffffu, u, 0);
+        ps = __shfl_sync(0xffffffffu, ps, 0);
+        pending_u = 0xffffffffu;
+        ++n_taken;
+        uint32_t item, fu = 0;
+        uint64_t src = 0, dst = 0, len = 0;
+        spec_lookup(spec, u, lane, item, fu, src, dst, len);
+        if (item == 0xffffffffu) {
+          item = find_item(ctx, u, cur, ps, lane);
+          if (item != 0xffffffffu) {
+            const Plan& p = ctx->plan[item % kPlanRing];
+            src = ld_cg64(&p.src); dst = ld_cg64(&p.dst); len = ld_cg64(&p.len);
+            fu = ld_cg32(&p.first_unit);
+            cur = item;
+          }
+        }
+        if (item == 0xffffffffu) {
+          exhausted = true;
+        } else {
+          const uint32_t c = u - fu;
+          const uint64_t lo = (uint64_t)c * chunk;
+          const uint64_t hi = min(len, lo + chunk);
+          const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src) + lo;
+          uint8_t* d8 = reinterpret_cast<uint8_t*>(dst) + lo;
+          const uint64_t n = hi > lo ? hi - lo : 0;
+          const bool aligned = ((((uintptr_t)s8) | ((uintptr_t)d8)) & 15) == 0;
+          const uint32_t n16 = aligned ? (uint32_t)(n & ~15ull) : 0u;
+          if (n16 < n) warp_copy(s8 + n16, d8 + n16, n - n16, lane);   // ragged tail / unaligned: LSU
+          __syncwarp();                     // lanes' stores precede the arrive issued later by lane 0
+          if (n16 == 0) {
+            if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);
+          } else {
+            if (lane == 0) {
+              const int s = (int)(k_issue % STAGES);
+              st[s].dst = reinterpret_cast<uint64_t>(d8);
+              st[s].n = n16;
+              st[s].item = item;
+              items[k_issue % (2 * STAGES)] = item;
+              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[s])), "r"(n16)
+                           : "memory");
+              asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                           ::"r"(smem_addr(bufs + (size_t)s * chunk)), "l"(s8), "r"(n16), "r"(smem_addr(&bar[s]))
+                           : "memory");
+            }
+            ++k_issue;
+          }
+          progress = true;
+        }
       }
-      wait_end = 0;
-      u = __shfl_sync(0xffffffffu, u, 0);
-      ps = __shfl_sync(0xffffffffu, ps, 0);
-      pending_u = 0xffffffffu;
-      ++n_taken;
-      uint32_t item, fu = 0;
-      uint64_t src = 0, dst = 0, len = 0;
-      spec_lookup(spec, u, lane, item, fu, src, dst, len);
-      if (item == 0xffffffffu) {
-        item = find_item(ctx, u, cur, ps, lane);
-        if (item == 0xffffffffu) { exhausted = true; break; }
-        const Plan& p = ctx->plan[item % kPlanRing];
-        src = ld_cg64(&p.src); dst = ld_cg64(&p.dst); len = ld_cg64(&p.len);
-        fu = ld_cg32(&p.first_unit);
-        cur = item;
-      }
-      const uint32_t c = u - fu;
-      const uint64_t lo = (uint64_t)c * chunk;
-      const uint64_t hi = min(len, lo + chunk);
-      const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src) + lo;
-      uint8_t* d8 = reinterpret_cast<uint8_t*>(dst) + lo;
-      const uint64_t n = hi > lo ? hi - lo : 0;
-      const bool aligned = ((((uintptr_t)s8) | ((uintptr_t)d8)) & 15) == 0;
-      const uint32_t n16 = aligned ? (uint32_t)(n & ~15ull) : 0u;
-      if (n16 < n) warp_copy(s8 + n16, d8 + n16, n - n16, lane);   // ragged tail / unaligned: LSU
-      if (n16 == 0) {                                                // nothing for the engine
-        __syncwarp();
-        if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);
-        continue;
-      }
-      __syncwarp();     // tail stores of the lanes precede the arrive issued later by lane 0
-      if (lane == 0) {
-        const int s = (int)(k_issue % STAGES);
-        st[s].dst = reinterpret_cast<uint64_t>(d8);
-        st[s].n = n16;
-        st[s].item = item;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[s])), "r"(n16)
-                     : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(smem_addr(bufs + (size_t)s * chunk)), "l"(s8), "r"(n16), "r"(smem_addr(&bar[s]))
-                     : "memory");
-      }
-      ++k_issue;
     }
-    if (k_done == k_issue) {
-      if (exhausted) break;
-      continue;
-    }
+    // ---- 2. the oldest loaded stage -> its store (non-blocking check)
     if (k_store < k_issue) {
-      // ---- oldest load complete -> bulk store to the (peer) ring
+      uint32_t ok = 0;
       if (lane == 0) {
         const int s = (int)(k_store % STAGES);
         const uint32_t par = (phase >> s) & 1u;
-        uint32_t ok = 0;
-        while (!ok)
-          asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                       : "=r"(ok) : "r"(smem_addr(&bar[s])), "r"(par) : "memory");
-        phase ^= 1u << s;
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                     ::"l"(st[s].dst), "r"(smem_addr(bufs + (size_t)s * chunk)), "r"(st[s].n) : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(smem_addr(&bar[s])), "r"(par) : "memory");
+        if (ok) {
+          phase ^= 1u << s;
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       ::"l"(st[s].dst), "r"(smem_addr(bufs + (size_t)s * chunk)), "r"(st[s].n) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
-      ++k_store;
-      __syncwarp();
-      continue;   // store every loaded stage before waiting on the oldest store
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (ok) { ++k_store; progress = true; }
     }
-    // ---- oldest store complete -> the entry's arrive counter
-    if (k_done < k_store && lane == 0) {
-      const uint32_t newer = k_store - k_done - 1;   // groups allowed to stay pending
-      switch (newer) {
-        case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
-        case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
-        case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
-        case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
-        case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
-        case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
-        case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
-        default: asm volatile("cp.async.bulk.wait_group 7;" ::: "memory"); break;
+    // ---- 3. free a stage once its store has read shared memory (when needed)
+    if (k_free < k_store && (k_issue - k_free == (uint32_t)STAGES || !progress)) {
+      if (lane == 0) bulk_wait_group_read<STAGES>(k_store - k_free - 1);
+      ++k_free;
+      progress = true;
+    }
+    // ---- 4. count completed stores (lazily: keep at most STAGES outstanding)
+    if (k_done < k_free && (k_store - k_done > (uint32_t)STAGES || !progress || exhausted)) {
+      if (lane == 0) {
+        bulk_wait_group<STAGES>(k_store - k_done - 1);
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // async-proxy writes before the generic release
+        red_release_gpu_add(&S->arrive[items[k_done % (2 * STAGES)] % kPlanRing], 1u);
       }
-      // async-proxy writes are complete; order them before the generic release
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      red_release_gpu_add(&S->arrive[st[k_done % STAGES].item % kPlanRing], 1u);
+      ++k_done;
+      progress = true;
     }
-    if (k_done < k_store) ++k_done;
     __syncwarp();
+    if (exhausted && k_done == k_issue) break;
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }

@@ -182,7 +182,11 @@ struct PutArgs {
   FaultSpec fault;            // test-only fault injection
 };
 
-constexpr int kEngineStages = 4;   // TMA engine: shared-memory stages of `chunk` bytes
+#ifndef B200RING_ENGINE_STAGES
+#define B200RING_ENGINE_STAGES 4
+#endif
+constexpr int kEngineStages = B200RING_ENGINE_STAGES;   // TMA engine: shared-memory stages of `chunk` bytes
+constexpr uint32_t kEngineSmem = 200u << 10;             // dynamic shared memory the stages may use
 
 struct GetArgs {
   uint8_t* ring;
