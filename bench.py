@@ -283,8 +283,22 @@ def bench_c2(args):
     assert (status == 0).all().item()
     v = R.parse_views(views.cpu().numpy())
     assert (v["status"] == 0).all()
-    t_put = np.frombuffer(v["header"][:, 56:64].tobytes(), dtype="<u8")
-    lat_us = (v["t_visible"].astype(np.int64) - t_put.astype(np.int64)) / 1e3
+    # loaded latency, pooled over >= 1,000 messages: a further
+    # streaming pass (outside the timed region) with one view buffer per step,
+    # first 10 % dropped as warm-up
+    lat_steps = 20
+    lviews = [torch.zeros(m * 128, dtype=torch.uint8, device="cuda") for _ in range(lat_steps)]
+    for i in range(lat_steps):
+        R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
+        R.ring_consume(ring, m, lviews[i], None, 0, 0, sc)
+    torch.cuda.synchronize()
+    lat_all = []
+    for lv in lviews:
+        vv = R.parse_views(lv.cpu().numpy())
+        tp = np.frombuffer(vv["header"][:, 56:64].tobytes(), dtype="<u8").astype(np.int64)
+        lat_all += ((vv["t_visible"].astype(np.int64) - tp) / 1e3).tolist()
+    lat_us = lat_all[len(lat_all) // 10:]
+    del lviews
 
     payload = m * plen * args.steps
     value = payload / (ms / 1e3) / 1e9
@@ -363,9 +377,9 @@ def bench_c2(args):
                    "streams": "put on one stream, consume on another; consume(s) overlaps put(s), "
                               "put(s+1) takes credit as consume(s) releases entries (device-side waits)"},
         "msgs_per_s": round(m * args.steps / (ms / 1e3), 1),
-        "latency_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99),
-                       "what": "t_visible - t_put of the last step's 64 messages (same GPU clock; batched put, "
-                               "so it includes the wait behind earlier messages of the batch)"},
+        "latency_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99), "samples": len(lat_us),
+                       "what": "loaded: t_visible - t_put over 20 streamed steps (first 10 % dropped; same GPU "
+                               "clock; batched put, so it includes the wait behind earlier messages of the batch)"},
         "kernels_ms": {"put_avg": round(put_avg_ms, 5), "consume_avg": round(statistics.mean(get_ms), 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("ncu_put_c2.json"),
@@ -462,9 +476,26 @@ def bench_pairs(args, rank, world, grp):
     ms = max(t0c.elapsed_time(t1c), t0p.elapsed_time(t1p), t0c.elapsed_time(t1p), t0p.elapsed_time(t1c))
     dist.barrier(group=grp)
     clocks = clk.stop() if clk else None
-    lat_loaded, v = latencies()
+    _, v = latencies()
     ok = bool((status == 0).all().item()) and bool((v["status"] == 0).all())
     log(f"timed region {ms:.3f} ms, ok = {ok}")
+    # loaded latency pooled over further streamed steps (outside the timed
+    # region), one view buffer per step, first 10 % dropped
+    lat_steps = 20
+    lviews = [torch.zeros(m * 128, dtype=torch.uint8, device="cuda") for _ in range(lat_steps)]
+    dist.barrier(group=grp)
+    for i in range(lat_steps):
+        R.ring_consume(ring, m, lviews[i], None, 0, 0, sc)
+        R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
+    torch.cuda.synchronize()
+    lat_loaded = []
+    prev_rank = (rank - 1) % world
+    for lv in lviews:
+        vv = R.parse_views(lv.cpu().numpy())
+        tp = np.frombuffer(vv["header"][:, 56:64].tobytes(), dtype="<u8").astype(np.int64)
+        lat_loaded += (((vv["t_visible"].astype(np.int64) - offsets[rank]) - (tp - offsets[prev_rank])) / 1e3).tolist()
+    lat_loaded = lat_loaded[len(lat_loaded) // 10:]
+    del lviews
 
     # unloaded latency: one message in flight (consumer waiting first), 4 KiB and one C3 tensor
     unl = {}
@@ -478,7 +509,7 @@ def bench_pairs(args, rank, world, grp):
             R.ring_put_batch(peer, one, 1, 0, status, sp)
             torch.cuda.synchronize()
             lv, vv = latencies()
-            if it >= 2 and int(vv["status"][0]) == 0:
+            if it >= args.lat_iters // 10 and int(vv["status"][0]) == 0:
                 lat.append(lv[0])
         unl[size] = lat
 
@@ -541,7 +572,8 @@ def bench_pairs(args, rank, world, grp):
             "unloaded_4MiB_p50": pct(u4m, 50), "unloaded_4MiB_p99": pct(u4m, 99),
             "samples": {"loaded": len(loaded), "unloaded_4KiB": len(u4k), "unloaded_4MiB": len(u4m)},
             "what": "t_visible (consumer GPU) - t_put (producer GPU), both %globaltimer mapped to the host "
-                    "CLOCK_MONOTONIC with ring_clock_offset_ns; loaded = last timed step"},
+                    "CLOCK_MONOTONIC with ring_clock_offset_ns; loaded = 20 streamed steps after the timed "
+                    "region, unloaded = one message in flight; first 10 % of each dropped"},
         "roofline": {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": NVLINK_PEAK_MEASURED, "unit": "GB/s",
                      "frac": round(per_gpu / NVLINK_PEAK_MEASURED, 4), "traffic": None, "kernel": "put_kernel",
                      "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal); "
@@ -601,7 +633,8 @@ def main():
                     help="fanin: the paper's locked MPSC ring, one SPSC ring per producer + ring_set_consume, "
                          "or a reserve-then-commit MPSC ring")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
-    ap.add_argument("--lat-iters", type=int, default=40)
+    ap.add_argument("--lat-iters", type=int, default=560,
+                    help="N>1: unloaded-latency round trips per size per rank (>= 1,000 samples pooled at N=2)")
     ap.add_argument("--no-overlap", action="store_true", help="N=1: put(s+1) waits for consume(s)")
     ap.add_argument("--graph", action="store_true",
                     help="N=1: replay a CUDA graph of 16 steps in the timed region (default: eager launches)")
