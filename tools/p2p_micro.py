@@ -29,13 +29,26 @@ for size in sizes:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.device(1):
                 e0.record(sc)
+            if os.environ.get("ONE_CONSUME"):          # one consumer launch for every step's messages
+                vall = torch.zeros(m * steps * 128, dtype=torch.uint8, device="cuda:1")
+                R.ring_consume(ring, m * steps, vall, None, 0, 0, sc)
             for s in range(steps):
-                R.ring_consume(ring, m, vw, None, 0, 0, sc)
+                if not os.environ.get("ONE_CONSUME"):
+                    R.ring_consume(ring, m, vw, None, 0, 0, sc)
                 R.ring_put_batch(peer, d, m, 0, st, sp)
             with torch.cuda.device(1):
                 e1.record(sc)
             torch.cuda.synchronize(0); torch.cuda.synchronize(1)
         ok = bool((st[:m] == 0).all().item())
+        if os.environ.get("B200RING_TRACE"):
+            t = R.ring_peer_trace(peer).astype(np.int64)
+            for nm, h in (("prev", t[2048:]), ("last", t[:2048])):
+                z = t[2048 + 252]
+                rel = lambda v: round((v - z) / 1e3, 1) if v else None
+                rounds = [(rel(h[4 * r]), rel(h[4 * r + 1]), int(h[4 * r + 3])) for r in range(64) if h[4 * r]]
+                fl = [(rel(h[256 + 2 * j]), int(h[257 + 2 * j])) for j in range(512) if h[256 + 2 * j]]
+                print(f"  {nm}: entry {rel(h[252])} end {rel(h[253])} rounds(start,placed,g) {rounds[:12]}")
+                print(f"  {nm}: flushes {fl[:40]}")
         ms = e0.elapsed_time(e1)
         print(f"size={size:>10} m={m:3d} ctas={ctas:4d} mode={mode} {m * steps * size / ms / 1e6:8.1f} GB/s ok={ok}",
               flush=True)
