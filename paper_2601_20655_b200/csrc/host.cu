@@ -627,7 +627,12 @@ static void default_grid(int device, bool sys, uint32_t* ctas, uint32_t* threads
   // faster (profiles/r01_threads_sweep.txt).  NVLink (sys) needs more in flight.
   if (!*threads) *threads = sys ? 512u : 256u;
   if (!*chunk) {
-    *chunk = 32u << 10;
+    // NVLink: 33 CTAs x 15 copy warps x 16 KiB keeps ~8 MB in flight -- the
+    // link's bandwidth x latency with room to spare; more in flight only
+    // spreads every message's units over a longer window, so messages complete
+    // (and free ring space) later: 32 KiB units lose ~6 % on the 64 MiB C3
+    // ring, 64-256 KiB up to 30 % (profiles/r01_nvlink_sweep.txt).
+    *chunk = sys ? 16u << 10 : 32u << 10;
     // tuning knob (power of two, 4 KiB .. 1 MiB)
     if (const char* e = getenv("B200RING_CHUNK")) {
       const unsigned long v = strtoul(e, nullptr, 0);

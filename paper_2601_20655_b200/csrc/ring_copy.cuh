@@ -24,14 +24,32 @@ __device__ __forceinline__ uint64_t ld_cg64(const uint64_t* p) { return __ldcg(r
 
 // Warp copy of `nb` bytes, lanes striding 16 B.
 __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8_t* dst, uint64_t nb, int lane) {
-  if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+#ifndef B200RING_COPY_U
+#define B200RING_COPY_U 16
+#endif
+#ifndef B200RING_COPY_V
+#define B200RING_COPY_V 2
+#endif
+  if (B200RING_COPY_V == 2 && (((uintptr_t)src | (uintptr_t)dst) & 31) == 0) {
+    // payloads start 64 B into a 128-B aligned entry: 32-B aligned whenever
+    // the source is
+    const uint32_t n32 = (uint32_t)(nb >> 5);
+    uint32_t i = lane;
+    constexpr int U = B200RING_COPY_U / 2;   // same 8 KiB in flight per warp
+    for (; i + (U - 1) * 32 < n32; i += U * 32) {
+      v8u32 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = ld_stream32(src + 32ull * (i + j * 32));
+#pragma unroll
+      for (int j = 0; j < U; ++j) st32(dst + 32ull * (i + j * 32), v[j]);
+    }
+    for (; i < n32; i += 32) st32(dst + 32ull * i, ld_stream32(src + 32ull * i));
+    for (uint64_t j = ((uint64_t)n32 << 5) + lane; j < nb; j += 32) dst[j] = src[j];
+  } else if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
     const int4* s = reinterpret_cast<const int4*>(src);
     int4* d = reinterpret_cast<int4*>(dst);
     const uint32_t n16 = (uint32_t)(nb >> 4);
     uint32_t i = lane;
-#ifndef B200RING_COPY_U
-#define B200RING_COPY_U 16
-#endif
     constexpr int U = B200RING_COPY_U;   // 16: 8 KiB in flight per warp
     for (; i + (U - 1) * 32 < n16; i += U * 32) {
       int4 v[U];

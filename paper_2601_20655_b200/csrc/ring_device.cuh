@@ -133,6 +133,23 @@ __device__ __forceinline__ int4 ld_stream16(const void* p) {
 __device__ __forceinline__ void st16(void* p, int4 v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
+// 32-byte accesses (LDG.256 / STG.256 on sm_100): half the instructions per
+// byte of the 16-byte ones; over NVLink the SM's store issue rate is what
+// limits a copy on a small grid (tools/p2p_ceiling.cu).
+struct alignas(32) v8u32 { uint32_t r[8]; };
+__device__ __forceinline__ v8u32 ld_stream32(const void* p) {
+  v8u32 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.r[0]), "=r"(v.r[1]), "=r"(v.r[2]), "=r"(v.r[3]), "=r"(v.r[4]), "=r"(v.r[5]), "=r"(v.r[6]),
+                 "=r"(v.r[7])
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st32(void* p, const v8u32& v) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.r[0]), "r"(v.r[1]), "r"(v.r[2]),
+               "r"(v.r[3]), "r"(v.r[4]), "r"(v.r[5]), "r"(v.r[6]), "r"(v.r[7])
+               : "memory");
+}
 
 __device__ __forceinline__ uint64_t warp_incl_scan64(uint64_t x, int lane) {
 #pragma unroll
