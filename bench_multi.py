@@ -229,6 +229,8 @@ def run_fanin(args, rank, world, grp, offsets):
                          "frac": round(best / NVLINK_PEAK_MEASURED, 4)},
             "config": {"workload": ("C5a variant (SURVEY.md sec 8 f3): GPUs 1..N-1 -> one 512 MiB SPSC ring each on GPU 0, "
                                     "one consumer warp" if lockfree else
+                                    "C5a variant (SURVEY.md sec 8 f3 ii): GPUs 1..N-1 -> one reserve-then-commit MPSC "
+                                    "ring on GPU 0, size sweep" if mode == "rc" else
                                     "C5a: GPUs 1..N-1 -> one MPSC ring (paper lock) on GPU 0, size sweep"),
                        "R_bytes": (512 << 20) if lockfree else 1 << 30, "n_slots": 256},
             "higher_is_better": True, "dtype": "u8", "data": "synthetic"}
