@@ -13,9 +13,24 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-cudart", "static", "--expt-relaxed-constexpr"]
 
 
+STAMP = LIB + ".flags"
+
+
+def _extra() -> list:
+    return os.environ.get("B200RING_NVCC_DEFINES", "").split()   # experiments only
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
+    # a library built with other experiment defines is stale too
+    try:
+        with open(STAMP) as f:
+            if f.read() != " ".join(_extra()):
+                return True
+    except OSError:
+        if _extra():
+            return True
     t = os.path.getmtime(LIB)
     for f in SOURCES + HEADERS:
         if os.path.getmtime(os.path.join(CSRC, f)) > t:
@@ -29,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        extra = os.environ.get("B200RING_NVCC_DEFINES", "").split()   # experiments only
+        extra = _extra()
         cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
@@ -40,6 +55,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.run([NVCC, "-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
                     *objs, "-o", tmp], check=True)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(_extra()))
     return LIB
 
 

@@ -1124,8 +1124,9 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
   }
 }
 
-// MODE 0: LSU copy warps; MODE 1: one TMA engine warp per CTA.  Two kernels,
-// so the TMA path's registers never change the LSU copy loop's code.
+// MODE 0: LSU copy warps; MODE 1: one TMA engine warp per CTA; MODE 2: LSU
+// copy warps with 32-B accesses (NVLink destinations).  Separate kernels, so
+// one path's registers never change another's copy loop.
 template <int MODE>
 __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
   LaunchCtx* ctx = a.ctx;
@@ -1139,7 +1140,7 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
     cs.owner = 0;
     // the block of first units of this CTA's copy warps (copy_mode 0)
     const uint32_t ncw = (blockDim.x >> 5) - (blockIdx.x == 0 ? 2u : 0u);
-    if (MODE == 0) cs.first = atomicAdd(&S->next_unit, ncw);
+    if (MODE != 1) cs.first = atomicAdd(&S->next_unit, ncw);
   }
   __syncthreads();
   if (blockIdx.x == 0) {
@@ -1173,7 +1174,7 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
   const uint32_t ncopy = blockDim.x - (blockIdx.x == 0 ? 64u : 0u);
   if (warp == (blockIdx.x == 0 ? 2 : 0)) spec_first_round(a, &spec);
   asm volatile("bar.sync 2, %0;" ::"r"(ncopy) : "memory");
-  copy_warp(ctx, S, &cs, a.chunk, a.timeout_ns, a.trace, &spec);
+  copy_warp<MODE == 2 ? 2 : 1>(ctx, S, &cs, a.chunk, a.timeout_ns, a.trace, &spec);
 }
 
 // With CUDA's lazy module loading, the first launch of a kernel loads it, and
@@ -1184,6 +1185,7 @@ cudaError_t preload_put() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, put_kernel<0>);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, put_kernel<1>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, put_kernel<2>);
   if (e == cudaSuccess)   // TMA engine stages (up to kEngineStages x 48 KiB)
     e = cudaFuncSetAttribute(put_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEngineSmem);
   return e;
@@ -1192,6 +1194,7 @@ cudaError_t preload_put() {
 cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s) {
   const size_t dyn = a.copy_mode == 1 ? (size_t)kEngineStages * a.chunk : 0;
   if (a.copy_mode == 1) put_kernel<1><<<ctas, 96u, dyn, s>>>(a);
+  else if (a.dest0.sys && !a.routes) put_kernel<2><<<ctas, threads, 0, s>>>(a);
   else put_kernel<0><<<ctas, threads, 0, s>>>(a);
   return cudaGetLastError();
 }

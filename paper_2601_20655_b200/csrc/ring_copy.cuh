@@ -23,16 +23,16 @@ __device__ __forceinline__ uint32_t ld_cg32(const uint32_t* p) { return __ldcg(p
 __device__ __forceinline__ uint64_t ld_cg64(const uint64_t* p) { return __ldcg(reinterpret_cast<const unsigned long long*>(p)); }
 
 // Warp copy of `nb` bytes, lanes striding 16 B.
-__device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8_t* dst, uint64_t nb, int lane) {
+// V = 2: 32-B accesses (LDG/STG.256) when both sides are 32-B aligned
+// (payloads start 64 B into a 128-B aligned entry, so whenever the source is):
+// +1.5 % over NVLink, but -12 % for HBM -> HBM (C2), so only the put kernel
+// instance for NVLink destinations uses it (profiles/r01_nvlink_sweep.txt).
 #ifndef B200RING_COPY_U
 #define B200RING_COPY_U 16
 #endif
-#ifndef B200RING_COPY_V
-#define B200RING_COPY_V 2
-#endif
-  if (B200RING_COPY_V == 2 && (((uintptr_t)src | (uintptr_t)dst) & 31) == 0) {
-    // payloads start 64 B into a 128-B aligned entry: 32-B aligned whenever
-    // the source is
+template <int V = 1>
+__device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8_t* dst, uint64_t nb, int lane) {
+  if (V == 2 && (((uintptr_t)src | (uintptr_t)dst) & 31) == 0) {
     const uint32_t n32 = (uint32_t)(nb >> 5);
     uint32_t i = lane;
     constexpr int U = B200RING_COPY_U / 2;   // same 8 KiB in flight per warp
@@ -125,6 +125,7 @@ __device__ __forceinline__ uint64_t wait_planned(LaunchSet* S, CopyShared* cs, u
 // After the control warp's release: one poller per CTA acquires it, then the
 // lanes read 32 candidate plans' copy sectors (unit range AND copy fields) in
 // one round trip; the hit lane broadcasts its fields.
+template <int V = 1>
 __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShared* cs, uint32_t chunk,
                                           uint64_t timeout_ns, uint64_t* trace = nullptr,
                                           const SpecRound* spec = nullptr) {
@@ -210,7 +211,7 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
     const uint64_t lo = (uint64_t)c * chunk;
     const uint64_t hi = min(len, lo + chunk);
     if (tr && lane == 0) tr[2] = globaltimer();
-    if (hi > lo) warp_copy(reinterpret_cast<const uint8_t*>(src) + lo, reinterpret_cast<uint8_t*>(dst) + lo, hi - lo, lane);
+    if (hi > lo) warp_copy<V>(reinterpret_cast<const uint8_t*>(src) + lo, reinterpret_cast<uint8_t*>(dst) + lo, hi - lo, lane);
     __syncwarp();
     if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);
     if (tr && lane == 0) tr[3] = globaltimer();
