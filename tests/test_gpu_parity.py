@@ -112,10 +112,12 @@ def test_c1_system_scope_same_device(R):
     assert img["tail"] == sim.mem.tail == img["head"]
 
 
-@pytest.mark.parametrize("copy_mode", [0, 1])
-def test_edge_sizes_and_unaligned_sources(R, copy_mode):
-    """Empty payload, sub-vector tails, exact fit f == R, and sources that are
-    not 16-B (or 4-B) aligned (the TMA engine falls back to the LSU for those)."""
+@pytest.mark.parametrize("copy_mode,local", [(0, True), (1, True), (0, False)])
+def test_edge_sizes_and_unaligned_sources(R, copy_mode, local):
+    """Empty payload, sub-vector tails, exact fit f == R, and sources aligned to
+    1, 4, 16 and 32 B (the TMA engine falls back to the LSU for unaligned ones;
+    a ring without RING_CREATE_LOCAL takes the NVLink put kernel, whose 32-B
+    loop falls back to 16-B, 4-B and byte copies)."""
     L = Layout(4096, 8)
     # f == R (4096 - 64 B payload) only fits an empty ring at P_b = 0 without
     # waiting for the consumer (one GPU runs put, then get), so it goes first.
@@ -124,18 +126,18 @@ def test_edge_sizes_and_unaligned_sources(R, copy_mode):
     stream = [synth.Message(0, q, n, *synth.header_fields(7, 0, q), payload=synth.payload_bytes(7, 0, q, n))
               for q, n in enumerate(lens)]
     sim = oracle_spsc(L, to_oracle_msgs(stream))
-    ring = R.ring_create(0, L.R, L.N, 1, R.RING_CREATE_LOCAL)
+    ring = R.ring_create(0, L.R, L.N, 1, R.RING_CREATE_LOCAL if local else 0)
     peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
     R.ring_bind_mirror(ring, 0, mh)
     R.ring_peer_config(peer, 0, 0, copy_mode)
-    host = np.zeros(sum(n + 32 for n in lens), dtype=np.uint8)
+    host = np.zeros(sum(n + 64 for n in lens), dtype=np.uint8)
     srcs_off, o = [], 0
     for q, m in enumerate(stream):
-        o += (1, 4, 0)[q % 3]                       # unaligned by 1, by 4, aligned
+        o += (1, 4, 16, 0)[q % 4]                   # aligned to 1, 4, 16, 32 B
         srcs_off.append(o)
         host[o:o + m.length] = m.payload
         o += m.length + 16
-        o = (o + 15) // 16 * 16
+        o = (o + 31) // 32 * 32
     buf = torch.from_numpy(host).cuda()
     msgs = msg_tensor(stream, [buf.data_ptr() + x for x in srcs_off], "cuda:0")
     got = []
