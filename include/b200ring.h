@@ -198,7 +198,10 @@ ring_status_t ring_put_batch(ring_peer_t peer, const ring_msg_t* d_msgs, uint32_
 ring_status_t ring_put(ring_peer_t peer, const void* d_payload, uint64_t len, const ring_hdr_t* hdr,
                        uint32_t flags, uint32_t* d_status, void* stream);
 /* Tuning: copy CTAs and threads per CTA of this attachment's put kernel
- * (0 = default), copy engine (0 = 16-B vector LSU, 1 = TMA bulk). */
+ * (0 = default: 148 x 256 with 32 KiB work units for a same-GPU ring,
+ * 33 x 512 with 16 KiB units across NVLink; threads <= 512), copy engine
+ * (0 = vector LSU -- 16-B accesses same-GPU, 32-B across NVLink -- or
+ * 1 = TMA bulk).  RING_EINVAL for values out of range. */
 ring_status_t ring_peer_config(ring_peer_t peer, uint32_t copy_ctas, uint32_t threads, uint32_t copy_mode);
 /* Host-side count of messages this attachment has submitted (= next header seq). */
 uint64_t ring_peer_submitted(ring_peer_t peer);

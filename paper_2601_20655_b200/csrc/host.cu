@@ -473,7 +473,7 @@ ring_status_t ring_detach(ring_peer_t p) {
 
 // ---- producer ----------------------------------------------------------------------
 ring_status_t ring_peer_config(ring_peer_t p, uint32_t copy_ctas, uint32_t threads, uint32_t copy_mode) {
-  if (!p || copy_ctas > 1023 || (threads && (threads % 32 || threads > 1024 || threads < 64)) || copy_mode > 1)
+  if (!p || copy_ctas > 1023 || (threads && (threads % 32 || threads > 512 || threads < 64)) || copy_mode > 1)
     return RING_EINVAL;
   p->copy_ctas = copy_ctas;
   p->threads = threads;
