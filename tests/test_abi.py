@@ -81,3 +81,13 @@ def test_binding_has_no_fallback(lib):
                 assert not re.search(r"#\s*include\s*[<\"].*oracle", src), f
                 assert "import synth" not in src and "from synth" not in src, f
     assert lib.LIB_PATH.startswith(pkg)
+
+
+def test_build_tracks_experiment_defines(lib, monkeypatch):
+    """A library built with other experiment defines (B200RING_NVCC_DEFINES)
+    counts as stale, so A/B builds never silently reuse the previous one."""
+    from paper_2601_20655_b200 import build
+    monkeypatch.delenv("B200RING_NVCC_DEFINES", raising=False)
+    assert not build._stale()
+    monkeypatch.setenv("B200RING_NVCC_DEFINES", "-DB200RING_COPY_U=8")
+    assert build._stale()
