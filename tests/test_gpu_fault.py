@@ -166,31 +166,38 @@ def test_torn_payload_rejected_by_payload_crc(R):
     assert v["status"] == R.RING_ECORRUPT and v["footprint"] == 384
 
 
-def test_fault_free_traffic_on_fault_tolerant_ring(R):
+@pytest.mark.parametrize("cross", [False, True])
+def test_fault_free_traffic_on_fault_tolerant_ring(R, cross):
     """No faults: two senders alternating on a fault-tolerant ring deliver every
     message exactly once, in per-channel order, byte-exact; slot words carry
-    the sequence tag (R21) and footprints as the fault-free oracle predicts."""
+    the sequence tag (R21) and footprints as the fault-free oracle predicts.
+    `cross`: both senders on GPU 1, the ring on GPU 0 (NVLink)."""
+    if cross and torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    sdev = 1 if cross else 0
     ring = R.ring_create(0, 1 << 16, 16, 2, R.RING_CREATE_FAULT_TOLERANT)
     lens = [[100, 4000, 0, 1000, 7000], [300, 64, 2000, 5000, 10]]
     senders = []
     for pid in (X, Y):
-        peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, pid)
+        peer, mh = R.ring_attach_peer(R.ring_export(ring), sdev, pid)
         R.ring_bind_mirror(ring, pid, mh)
         R.ring_peer_config(peer, 2, 256, 0)
         pays = [synth.payload_bytes(synth.SEED_BASE + 41, pid, k, n).tobytes() for k, n in enumerate(lens[pid])]
-        buf = torch.zeros(sum((n + 255) // 256 * 256 for n in lens[pid]) + 256, dtype=torch.uint8, device="cuda")
+        buf = torch.zeros(sum((n + 255) // 256 * 256 for n in lens[pid]) + 256, dtype=torch.uint8,
+                          device=f"cuda:{sdev}")
         srcs, o = [], 0
         for p in pays:
             buf[o:o + len(p)] = torch.frombuffer(bytearray(p), dtype=torch.uint8) if p else buf[o:o]
             srcs.append(buf.data_ptr() + o)
             o += (len(p) + 255) // 256 * 256
         a = R.make_msgs(srcs, lens[pid], [bytes(16)] * 5, [0] * 5, [0] * 5, [0] * 5)
-        senders.append((peer, torch.from_numpy(a.view(np.uint8).copy()).cuda(), pays, buf))
-    st = [torch.full((5,), 10, dtype=torch.int32, device="cuda") for _ in range(2)]
-    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        senders.append((peer, torch.from_numpy(a.view(np.uint8).copy()).cuda(sdev), pays, buf))
+    st = [torch.full((5,), 10, dtype=torch.int32, device=f"cuda:{sdev}") for _ in range(2)]
+    streams = [torch.cuda.Stream(sdev), torch.cuda.Stream(sdev)]
     for pid in (X, Y):
         R.ring_put_batch(senders[pid][0], senders[pid][1], 5, 0, st[pid], streams[pid])
-    torch.cuda.synchronize()
+    torch.cuda.synchronize(sdev)
+    torch.cuda.synchronize(0)
     assert all((s == 0).all().item() for s in st)
     views = torch.zeros(10 * 128, dtype=torch.uint8, device="cuda")
     R.ring_get(ring, 10, views, None, 0, R.RING_TRY)
