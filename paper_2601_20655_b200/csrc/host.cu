@@ -624,8 +624,12 @@ static void default_grid(int device, bool sys, uint32_t* ctas, uint32_t* threads
   // every unit then completes at the very end of the launch and the consumer
   // cannot release (and the next put cannot place) anything earlier.  With 8
   // warps units complete in waves, in order, and the streaming C2 step is ~10%
-  // faster (profiles/r01_threads_sweep.txt).  NVLink (sys) needs more in flight.
-  if (!*threads) *threads = sys ? 512u : 256u;
+  // faster (profiles/r01_threads_sweep.txt).  7 warps rather than 8: the C2
+  // launch's 2,048 units of 32 KiB then take almost exactly two rounds of the
+  // 1,034 copy warps instead of 1.7 rounds of 1,182, and the streaming step is
+  // ~5 % faster (profiles/r01_c2_grid_sweep.txt).  NVLink (sys) needs more in
+  // flight.
+  if (!*threads) *threads = sys ? 512u : 224u;
   if (!*chunk) {
     // NVLink: 33 CTAs x 15 copy warps x 16 KiB keeps ~8 MB in flight -- the
     // link's bandwidth x latency with room to spare; more in flight only
