@@ -155,7 +155,8 @@ typedef struct {
  * ring_create: allocate and zero one ring on `device` (lock
  * region, header with head/tail, buffer region of `data_bytes` = R bytes, size
  * region of `n_slots` = N slots).  R must be a positive multiple of 128 below
- * 2^40; N a power of two <= 2^23; 1 <= max_producers <= 64.  With
+ * 2^39 (R8: packed pointer words; bit 63 of a mirror word marks it bound);
+ * N a power of two <= 2^23; 1 <= max_producers <= 64.  With
  * max_producers == 1 the lock is elided (R14).  Layout: DESIGN.md §3. */
 ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uint32_t max_producers,
                           uint32_t flags, ring_t* out);
@@ -304,13 +305,16 @@ ring_status_t ring_get(ring_t ring, uint32_t n, ring_view_t* d_views, void* d_ds
  * the number held is clamped. */
 ring_status_t ring_release(ring_t ring, uint32_t count, void* stream);
 /* ring_consume: ring_get + ring_release of each entry as soon as it has been
- * read (and copied, if d_dst != NULL): the paper's receiver loop as one launch. */
+ * read (and copied, if d_dst != NULL): the paper's receiver loop as one launch.
+ * Entries still held from an earlier ring_get are released first (in order). */
 ring_status_t ring_consume(ring_t ring, uint32_t n, ring_view_t* d_views, void* d_dst, uint64_t dst_stride,
                            uint32_t flags, void* stream);
 /* Tuning: CTAs / threads of the copy-out get (0 = default).  A copy-out get
  * and a put on the SAME GPU spin on each other: one CTA of each must fit on an
  * SM together (the defaults do: ~23 K + ~27 K registers); a get grid of 512
- * threads per CTA does not, and the pair then only ends by timing out. */
+ * threads per CTA does not, and the pair then only ends by timing out.
+ * RING_EINVAL: threads > 512 (the kernel's launch bound), not a multiple of 32,
+ * or a one-CTA grid with fewer than 96 threads (no copy warp). */
 ring_status_t ring_config(ring_t ring, uint32_t copy_ctas, uint32_t threads);
 
 /* ---- inspection (tests, debugging; synchronous) ---------------------------------

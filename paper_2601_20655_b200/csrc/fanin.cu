@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(32) set_consume_kernel(const SetArgs a) {
     const uint32_t q = (ptr_seq(Gr) + e) & kSeqMask;
     uint64_t w = 0;
     if (act) w = ld_relaxed<SYS>(reinterpret_cast<const uint64_t*>(rg.ring + kSlotsOff) + (q & (rg.N - 1)));
-    const uint64_t f = act ? (w & ((1ull << 40) - 1)) : 0;
+    const uint64_t f = act ? (w & kFLow) : 0;
     const bool pad = act && (w & kPad);
     // segmented prefix sum of footprints within each ring's lanes
     uint64_t incl = f;

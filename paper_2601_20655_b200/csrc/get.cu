@@ -85,7 +85,7 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
     uint64_t w = 0;
     if ((uint32_t)lane < e) w = ld_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(G) + lane));
     // footprint: bits 0-39 (fault-tolerant rings keep a sequence tag in 40-61, R21; R < 2^40)
-    const uint64_t f = (uint32_t)lane < e ? (w & ((1ull << 40) - 1)) : 0;
+    const uint64_t f = (uint32_t)lane < e ? (w & kFLow) : 0;
     const bool pad = (w & kPad) != 0;
     const bool ismsg = (uint32_t)lane < e && !pad;
     const uint64_t incl = warp_incl_scan64(f, lane);
@@ -153,12 +153,15 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
     if (copy) {
       // ---- one item per entry; the copy warps move the payloads
       const uint32_t inmask = __ballot_sync(0xffffffffu, in);
+      uint32_t flow_to = 0;
       if (lane == 0 && items + e2 - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing) {
         const uint64_t end = globaltimer() + 2 * a.timeout_ns;
         while (items + e2 - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing)
-          if (globaltimer() > end) break;
+          if (globaltimer() > end) { flow_to = 1; break; }
       }
-      __syncwarp();
+      // Plan slots still in use by the copy warps / finisher are never
+      // overwritten: on a flow-control timeout the batch is left unread.
+      if (__shfl_sync(0xffffffffu, flow_to, 0)) { fail = RING_ETIMEDOUT; break; }
       uint32_t nu = (in && deliver) ? units_for(len, a.chunk) : 0;
       uint32_t nu_incl = nu;
 #pragma unroll
@@ -283,6 +286,10 @@ __device__ void get_finisher(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S) {
 }
 
 template <bool SYS>
+__device__ void release_held(uint8_t* ring, uint64_t** mirrors, uint32_t n_mirrors, uint64_t R, uint32_t N,
+                             uint32_t count);
+
+template <bool SYS>
 __global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
   LaunchCtx* ctx = a.ctx;
   LaunchSet* S = &ctx->set[a.launch & 1];
@@ -290,6 +297,11 @@ __global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
   __shared__ uint32_t s_crc[kCrcTableWords];
   __shared__ CopyShared cs;
   if (threadIdx.x == 0) {
+    // ring_consume after a ring_get that left entries held: release them
+    // first (in order), so the head stays on entry boundaries; the control
+    // and finisher warps read the head after the CTA barrier below.
+    if (blockIdx.x == 0 && a.consume && *g_cursor(a.ring) != *g_head(a.ring))
+      release_held<SYS>(a.ring, a.mirrors, a.n_mirrors, a.R, a.N, 0xffffffffu);
     cs.pl = 0;
     cs.owner = 0;
     if (a.dst) cs.first = atomicAdd(&S->next_unit, (blockDim.x >> 5) - (blockIdx.x == 0 ? 2u : 0u));
@@ -311,25 +323,31 @@ __global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
 }
 
 // In-order release of `count` received entries plus the PAD entries the read
-// cursor has passed (R13): receiver steps 4-5.
+// cursor has passed (R13): receiver steps 4-5.  One thread.
 template <bool SYS>
-__global__ void release_kernel(const ReleaseArgs a) {
-  if (threadIdx.x != 0) return;
-  uint64_t H = *g_head(a.ring);
-  const uint64_t G = *g_cursor(a.ring);
-  uint32_t count = a.count;
+__device__ void release_held(uint8_t* ring, uint64_t** mirrors, uint32_t n_mirrors, uint64_t R, uint32_t N,
+                             uint32_t count) {
+  uint64_t H = *g_head(ring);
+  const uint64_t G = *g_cursor(ring);
   bool moved = false;
   while (ptr_seq(H) != ptr_seq(G)) {
-    const uint64_t w = ld_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(H)));
+    const uint64_t w = ld_relaxed<SYS>(g_slot(ring, N, ptr_seq(H)));
     if (!(w & kPad)) {
       if (count == 0) break;
       --count;
     }
-    st_relaxed<SYS>(g_slot(a.ring, a.N, ptr_seq(H)), 0ull);
-    H = pack_ptr(advance(ptr_off(H), w & kFMask, a.R), seq_inc(ptr_seq(H)));
+    st_relaxed<SYS>(g_slot(ring, N, ptr_seq(H)), 0ull);
+    // footprint bits 0-39: a fault-tolerant ring's slots carry a tag above (R21)
+    H = pack_ptr(advance(ptr_off(H), w & kFLow, R), seq_inc(ptr_seq(H)));
     moved = true;
   }
-  if (moved) publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
+  if (moved) publish_head<SYS>(ring, mirrors, n_mirrors, H);
+}
+
+template <bool SYS>
+__global__ void release_kernel(const ReleaseArgs a) {
+  if (threadIdx.x != 0) return;
+  release_held<SYS>(a.ring, a.mirrors, a.n_mirrors, a.R, a.N, a.count);
 }
 
 cudaError_t preload_get() {   // see preload_put (put.cu)

@@ -475,6 +475,8 @@ ring_status_t ring_detach(ring_peer_t p) {
 ring_status_t ring_peer_config(ring_peer_t p, uint32_t copy_ctas, uint32_t threads, uint32_t copy_mode) {
   if (!p || copy_ctas > 1023 || (threads && (threads % 32 || threads > 512 || threads < 64)) || copy_mode > 1)
     return RING_EINVAL;
+  // CTA 0 holds the leader and publisher warps: a one-CTA LSU grid needs a third warp to copy
+  if (copy_mode == 0 && copy_ctas == 1 && threads && threads < 96) return RING_EINVAL;
   p->copy_ctas = copy_ctas;
   p->threads = threads;
   p->copy_mode = copy_mode;
@@ -703,7 +705,10 @@ ring_status_t ring_put(ring_peer_t p, const void* d_payload, uint64_t len, const
 
 // ---- consumer ----------------------------------------------------------------------
 ring_status_t ring_config(ring_t r, uint32_t copy_ctas, uint32_t threads) {
-  if (!r || copy_ctas > 1023 || (threads && (threads % 32 || threads > 1024 || threads < 64))) return RING_EINVAL;
+  // get_kernel is __launch_bounds__(512, 1); CTA 0 holds the control and
+  // finisher warps, so a one-CTA grid needs a third warp to copy
+  if (!r || copy_ctas > 1023 || (threads && (threads % 32 || threads > 512 || threads < 64))) return RING_EINVAL;
+  if (copy_ctas == 1 && threads && threads < 96) return RING_EINVAL;
   r->copy_ctas = copy_ctas;
   r->threads = threads;
   return RING_OK;
@@ -843,7 +848,9 @@ ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, cons
   nr.n = (uint16_t)n;
   for (uint32_t i = 0; i < n; ++i) {
     ring_peer_t p = dests[i];
-    if (!p || p->device != r->device) return RING_EINVAL;
+    // A routed put runs the batched (non-fault-tolerant) sender: it must never
+    // write untagged slots or hold a plain lock on a fault-tolerant ring.
+    if (!p || p->device != r->device || p->desc.ft) return RING_EINVAL;
     uint32_t idx = 0;
     while (idx < r->dests.size() && r->dests[idx] != p) ++idx;
     if (idx == r->dests.size()) {

@@ -62,6 +62,7 @@ struct LeaderState {
   uint32_t items, units;
   bool aborted;
   bool dead;                        // fault injection (reserve-then-commit): the sender is lost
+  bool flow_to;                     // plan-ring flow control timed out: plan slots may still be in use
   uint64_t me;                      // reserve-then-commit: this round's lock word
 };
 
@@ -85,9 +86,6 @@ struct MsgBrief {        // the fields lane 0 needs, computed in parallel by all
   uint64_t t_arr;        // arrival time (hdr.accepted_at): fast-reject admission
 };
 
-constexpr int kTagShift = 40;
-constexpr uint64_t kTagMask = (1ull << 22) - 1;
-constexpr uint64_t kFLow = (1ull << kTagShift) - 1;
 __device__ __forceinline__ uint64_t tagged_word(uint64_t w, uint32_t q) { return w | ((q & kTagMask) << kTagShift); }
 
 template <bool SYS>
@@ -248,7 +246,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
           if (seq_dist(ptr_seq(P), ptr_seq(H)) >= D.N) break;
           const uint64_t w = D.sys ? ld_relaxed<true>(slot_w(D, ptr_seq(P))) : ld_relaxed<false>(slot_w(D, ptr_seq(P)));
           if (!(w & kBusy)) break;
-          P = pack_ptr(advance(ptr_off(P), w & kFMask, D.R), seq_inc(ptr_seq(P)));
+          P = pack_ptr(advance(ptr_off(P), w & kFLow, D.R), seq_inc(ptr_seq(P)));
           if (D.sys) st_release<true>(tail_w(D), P); else st_release<false>(tail_w(D), P);
         }
         held = (int)d;
@@ -705,6 +703,7 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     L.units = 0;
     L.aborted = false;
     L.dead = false;
+    L.flow_to = false;
   }
   __syncwarp();
   for (uint32_t k0 = 0; k0 < a.n;) {
@@ -731,7 +730,7 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
           L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing) {
         const uint64_t end = globaltimer() + 2 * a.timeout_ns;
         while (L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing)
-          if (globaltimer() > end) { L.aborted = true; break; }
+          if (globaltimer() > end) { L.aborted = true; L.flow_to = true; break; }
       }
       const uint32_t rnd = k0 / kGroup;
       if (a.trace && rnd < 64) a.trace[rnd * 4] = globaltimer();
@@ -746,6 +745,12 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
       }
     }
     __syncwarp();
+    if (L.flow_to) {
+      // Plan slots the copy warps / publisher may still read are never
+      // overwritten: the remaining messages time out without a plan item.
+      for (uint32_t k = k0 + lane; k < a.n; k += 32) a.status[k] = RING_ETIMEDOUT;
+      break;
+    }
     uint32_t g = 0;
     if (fast && !L.aborted) g = fast_place(a, ctx, L, gmax, gs, brief, a.dest0);
     if (g == 0) {
@@ -1006,7 +1011,7 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
       if (D.sys) fence_acq_rel<true>(); else fence_acq_rel<false>();
       bool committed = false;
       if (mine && (flags & kEntry) && !(slot_word & kPad)) {
-        const uint64_t want = kResvBit | (slot_word & ((1ull << 40) - 1));
+        const uint64_t want = kResvBit | (slot_word & kFLow);
         committed = dcas(D, slot_w(D, slot), want, slot_word) == want;
         if (!committed) {
           a.status[ld_cg32(&ctx->plan[j % kPlanRing].msg)] = RING_EDROPPED;   // reservation taken (TL)

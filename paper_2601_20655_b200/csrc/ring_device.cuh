@@ -23,7 +23,12 @@ constexpr uint64_t kAlign = 128;     // entry alignment (R11)
 constexpr uint64_t kHdr = 64;        // entry header bytes (R11)
 constexpr uint64_t kBusy = 1ull << 63;
 constexpr uint64_t kPad = 1ull << 62;
-constexpr uint64_t kFMask = (1ull << 62) - 1;
+// Footprint bits of a size slot: 0-39 (R < 2^39, R8).  Fault-tolerant rings
+// keep a 22-bit sequence tag in bits 40-61 (R21), so every reader masks the
+// footprint with kFLow, never with the full 62 bits.
+constexpr int kTagShift = 40;
+constexpr uint64_t kTagMask = (1ull << 22) - 1;
+constexpr uint64_t kFLow = (1ull << kTagShift) - 1;
 constexpr uint64_t kResvBit = 1ull << 61;   // reserve-then-commit: slot claimed, entry not committed yet
 constexpr uint64_t kResvOff = 64;          // reservation frontier word (lock line; written under the lock)
 constexpr uint32_t kSeqMask = (1u << 24) - 1;

@@ -7,6 +7,7 @@ import numpy as np
 import torch
 
 import synth
+from synth import device as SD
 from oracle.ring import Layout, Sim, Msg, run, encode_header, decode_header
 from paper_2601_20655_b200 import ring as R
 
@@ -82,3 +83,85 @@ def check_views_against_oracle(views: np.ndarray, sim: Sim, first: int, stream, 
         assert hdr[:56] == d.header[:56]
         assert int(v["len"]) == m.length
         assert int(v["offset"]) == d.start + 64
+
+
+def devices(k: int, cross: bool) -> list[int]:
+    """k device ids: distinct GPUs when `cross` (skips the test if there are
+    fewer), else all on GPU 0 -- rings created without RING_CREATE_LOCAL then
+    take the system-scope (NVLink) kernels with producer and consumer kernels
+    spinning concurrently on one GPU."""
+    import pytest
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    if cross:
+        if torch.cuda.device_count() < k:
+            pytest.skip(f"needs {k} GPUs")
+        return list(range(k))
+    return [0] * k
+
+
+def device_sources(specs, seed: int, device="cuda"):
+    """Payload sources generated on the device: specs = [(channel, seq, length)];
+    one buffer with 256-B aligned offsets, filled with synth.payload_bytes of
+    each (seed, channel, seq).  Returns (buffer, [device addresses])."""
+    offs, total = [], 0
+    for _, _, n in specs:
+        offs.append(total)
+        total += (n + 255) // 256 * 256
+    buf = torch.empty(max(total, 256), dtype=torch.uint8, device=device)
+    ptrs = [buf.data_ptr() + o for o in offs]
+    with torch.cuda.device(buf.device):
+        keep = SD.fill(ptrs, [n for _, _, n in specs], [c for c, _, _ in specs], [q for _, q, _ in specs], seed)
+        torch.cuda.synchronize()
+    del keep
+    return buf, ptrs
+
+
+def dev_u64(vals, device="cuda") -> torch.Tensor:
+    return torch.tensor([v - 2**64 if v >= 2**63 else v for v in vals], dtype=torch.int64, device=device)
+
+
+def verify_views(ring, vt: torch.Tensor, n: int, seed: int, chans=None, seqs=None, stream=None, lut=None,
+                 lut_stride=0):
+    """On-device, exact compare of the payloads that n view records point at
+    (inside the ring: view mode, before release) with the seeded generator.
+    Keys default to the header's (producer_id, seq) [R11 bytes 44-52]; pass
+    device tensors to key otherwise, or a device table `lut` that maps the
+    header's (producer_id, seq) to the generator's seq: lut[pid * lut_stride +
+    seq].  Only device work on `stream` (no host synchronisation).  Returns the
+    device tensor of first-bad offsets (-1 = ok)."""
+    base = R.ring_get_info(ring).data
+    s = stream if stream is not None else torch.cuda.current_stream(vt.device)
+    with torch.cuda.device(vt.device), torch.cuda.stream(s):
+        raw = vt[: n * 128]
+        q = raw.view(torch.int64).view(n, 16)
+        w = raw.view(torch.int32).view(n, 32)
+        ptr = q[:, 0] + base
+        ln = q[:, 1]
+        ch = w[:, 27] if chans is None else chans
+        sq = w[:, 28].to(torch.int64) if seqs is None else seqs
+        if lut is not None:
+            sq = lut[ch.to(torch.int64) * lut_stride + sq]
+        return SD.verify(ptr, ln, ch, sq, seed, s)
+
+
+def replay_mpsc(L, progs, order, check=True):
+    """Oracle run that follows an observed lock order (R16): only the producer
+    whose message is next may step until that message is published; the
+    consumer drains whenever it can."""
+    sim = Sim(L, progs, mpsc=True, block=True, depth=1, check=check)
+    for pid in order:
+        p = sim.producers[pid]
+        target = len(p.outcomes) + 1
+        # until the message is published AND the lock released (Unlock follows UH)
+        while len(p.outcomes) < target or p.pc not in ("Lock", "DONE"):
+            if sim.producer_enabled(p):
+                sim.step(pid)
+            elif "Z" in sim.enabled():
+                sim.step("Z")
+            elif "Zrel" in sim.enabled():
+                sim.step("Zrel")
+            else:
+                raise AssertionError("replay stuck")
+    run(sim, policy="drain")
+    return sim

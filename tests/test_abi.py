@@ -91,3 +91,17 @@ def test_build_tracks_experiment_defines(lib, monkeypatch):
     assert not build._stale()
     monkeypatch.setenv("B200RING_NVCC_DEFINES", "-DB200RING_COPY_U=8")
     assert build._stale()
+
+
+def test_device_generator_matches_synth():
+    """The device payload generator (synth/csrc/synth_dev.cu, test infrastructure)
+    computes the same words as synth.payload_bytes: checked through its host
+    entry point for several keys, word indices and a ragged length."""
+    import numpy as np
+    import synth
+    from synth import device as sd
+    sd.build()
+    for seed, ch, seq in [(synth.SEED_BASE, 0, 0), (synth.SEED_BASE + 5, 2, 17), (1, 2**32 - 1, 2**48 + 3)]:
+        ref = synth.payload_bytes(seed, ch, seq, 8 * 40 + 3)
+        words = np.array([sd.word(seed, ch, seq, i) for i in range(41)], dtype=np.uint64)
+        assert words.view(np.uint8)[: ref.size].tobytes() == ref.tobytes()

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 import synth  # noqa: E402
 from oracle.ring import Layout, Sim, Msg, run, decode_header  # noqa: E402
 from gpu_util import (to_oracle_msgs, oracle_spsc, upload, msg_tensor, batches, views_host,  # noqa: E402
-                            check_views_against_oracle, expected_header)
+                      check_views_against_oracle, expected_header, replay_mpsc, devices)
 
 
 def _need(n):
@@ -256,28 +256,6 @@ def test_try_get_empty_and_block_timeout(R):
     R.ring_destroy(ring)
 
 
-def _replay_mpsc(L, progs, order):
-    """Oracle run that follows an observed lock order (R16): only the producer
-    whose message is next may step until that message is published; the
-    consumer drains whenever it can."""
-    sim = Sim(L, progs, mpsc=True, block=True, depth=1)
-    for pid in order:
-        p = sim.producers[pid]
-        target = len(p.outcomes) + 1
-        # until the message is published AND the lock released (Unlock follows UH)
-        while len(p.outcomes) < target or p.pc not in ("Lock", "DONE"):
-            if sim.producer_enabled(p):
-                sim.step(pid)
-            elif "Z" in sim.enabled():
-                sim.step("Z")
-            elif "Zrel" in sim.enabled():
-                sim.step("Zrel")
-            else:
-                raise AssertionError("replay stuck")
-    run(sim, policy="drain")
-    return sim
-
-
 def test_mpsc_three_producers_one_device(R):
     """Three attachments (lock taken per message, PAPER.md:697) put in turn;
     per-channel order exact; placements = the oracle replaying the observed order."""
@@ -319,7 +297,7 @@ def test_mpsc_three_producers_one_device(R):
         seqs = [decode_header(bytes(x["header"]))["seq"] for x in v
                 if decode_header(bytes(x["header"]))["producer_id"] == pid]
         assert seqs == list(range(24))
-    sim = _replay_mpsc(L, {pid: to_oracle_msgs(progs_stream[pid]) for pid in range(3)}, order)
+    sim = replay_mpsc(L, {pid: to_oracle_msgs(progs_stream[pid]) for pid in range(3)}, order)
     for x, d in zip(v, sim.cons.delivered):
         assert (int(x["start"]), int(x["footprint"]), int(x["slot_seq"])) == (d.start, d.f, d.seq_slot)
         assert bytes(x["header"])[:56] == d.header[:56]
@@ -421,55 +399,57 @@ def _p2p_stream(R, L, stream, prod_dev, cons_dev, cap, copy=True, copy_mode=0):
     return v, pl, _status(st), img
 
 
-@pytest.mark.multigpu
-def test_p2p_small_ring_streaming_wraps(R):
+@pytest.mark.parametrize("cross", [False, pytest.param(True, marks=pytest.mark.multigpu)])
+def test_p2p_small_ring_streaming_wraps(R, cross):
     """C1's stream over NVLink with producer and consumer concurrently spinning:
     1,000 messages through an 8-slot 32-KiB ring (~130 laps, credit via the
-    mirror, PAD entries at every wrap) in ONE put launch and ONE consume launch."""
-    _need(2)
+    mirror, PAD entries at every wrap) in ONE put launch and ONE consume launch.
+    cross=False: the same system-scope kernels on one GPU, two streams."""
+    prod, cons = devices(2, cross)
     L = Layout(32768, 8)
     stream = synth.random_stream(synth.SEED_BASE + 1, 0, 1000, 1, 4096)
     sim = oracle_spsc(L, to_oracle_msgs(stream))
-    v, pl, st, img = _p2p_stream(R, L, stream, 0, 1, 4096)
+    v, pl, st, img = _p2p_stream(R, L, stream, prod, cons, 4096)
     assert st == [0] * 1000
     check_views_against_oracle(v, sim, 0, stream)
     assert pl == [m.payload.tobytes() for m in stream]
     assert img["tail"] == sim.mem.tail == img["head"]
 
 
-@pytest.mark.multigpu
+@pytest.mark.parametrize("cross", [False, pytest.param(True, marks=pytest.mark.multigpu)])
 @pytest.mark.parametrize("copy_mode", [0, 1])
-def test_p2p_c3_wan_tensors(R, copy_mode):
+def test_p2p_c3_wan_tensors(R, copy_mode, cross):
     """BASELINE.json configs[2]: umT5 embeddings 512x4096 bf16 (4,194,304 B)
     alternating with 480p latents 16x21x60x104 bf16 (4,193,280 B), GPU0 -> ring
     on GPU1 (R = 64 MiB, N = 64), 48 messages in one streaming launch pair."""
-    _need(2)
+    prod, cons = devices(2, cross)
     L = Layout(64 << 20, 64)
     stream = synth.wan_stream(synth.SEED_BASE + 3, 0, 48)
     sim = oracle_spsc(L, to_oracle_msgs(stream))
-    v, pl, st, img = _p2p_stream(R, L, stream, 0, 1, 4194304, copy_mode=copy_mode)
+    v, pl, st, img = _p2p_stream(R, L, stream, prod, cons, 4194304, copy_mode=copy_mode)
     assert st == [0] * 48
     check_views_against_oracle(v, sim, 0, stream)
     assert pl == [m.payload.tobytes() for m in stream]
 
 
-@pytest.mark.multigpu
-def test_p2p_reverse_direction(R):
-    _need(2)
+@pytest.mark.parametrize("cross", [False, pytest.param(True, marks=pytest.mark.multigpu)])
+def test_p2p_reverse_direction(R, cross):
+    cons, prod = devices(2, cross)
     L = Layout(1 << 20, 16)
     stream = synth.random_stream(synth.SEED_BASE + 4, 0, 200, 1, 70000)
     sim = oracle_spsc(L, to_oracle_msgs(stream))
-    v, pl, st, img = _p2p_stream(R, L, stream, 1, 0, 70016)
+    v, pl, st, img = _p2p_stream(R, L, stream, prod, cons, 70016)
     check_views_against_oracle(v, sim, 0, stream)
     assert pl == [m.payload.tobytes() for m in stream]
 
 
-@pytest.mark.multigpu
-def test_mpsc_fan_in_three_gpus(R):
+@pytest.mark.parametrize("cross", [False, pytest.param(True, marks=pytest.mark.multigpu)])
+def test_mpsc_fan_in_three_gpus(R, cross):
     """C5 shape at small scale: producers on GPUs 1..3 -> one shared MPSC ring on
     GPU0 (paper lock), all concurrent; per-channel order exact, observed merge
-    replayed by the oracle."""
-    _need(4)
+    replayed by the oracle.  cross=False: three producer streams and the
+    consumer stream on one GPU, system-scope ring."""
+    devs = devices(4, cross)
     L = Layout(1 << 20, 32)
     n = 150
     streams = {pid: synth.random_stream(synth.SEED_BASE + 6, pid, n, 1, 40000) for pid in range(3)}
@@ -477,7 +457,7 @@ def test_mpsc_fan_in_three_gpus(R):
     h = R.ring_export(ring)
     peers, bufs, tens, sts, strs = [], [], [], [], []
     for pid in range(3):
-        dev = pid + 1
+        dev = devs[pid + 1]
         pe, mh = R.ring_attach_peer(h, dev, pid)
         R.ring_bind_mirror(ring, pid, mh)
         peers.append(pe)
@@ -493,7 +473,7 @@ def test_mpsc_fan_in_three_gpus(R):
     R.ring_consume(ring, 3 * n, vt, dst, cap, 0, sc)
     for pid in range(3):
         R.ring_put_batch(peers[pid], tens[pid], n, 0, sts[pid], strs[pid])
-    for dev in range(4):
+    for dev in set(devs):
         torch.cuda.synchronize(dev)
     for pid in range(3):
         assert _status(sts[pid]) == [0] * n
@@ -506,7 +486,7 @@ def test_mpsc_fan_in_three_gpus(R):
     for j, hh in enumerate(hdrs):
         m = streams[hh["producer_id"]][hh["seq"]]
         assert d[j * cap: j * cap + int(v[j]["len"])].tobytes() == m.payload.tobytes()
-    sim = _replay_mpsc(L, {pid: to_oracle_msgs(streams[pid]) for pid in range(3)}, order)
+    sim = replay_mpsc(L, {pid: to_oracle_msgs(streams[pid]) for pid in range(3)}, order)
     for x, dd in zip(v, sim.cons.delivered):
         assert (int(x["start"]), int(x["footprint"]), int(x["slot_seq"])) == (dd.start, dd.f, dd.seq_slot)
     img = R.ring_read_image(ring)

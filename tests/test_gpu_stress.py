@@ -1,4 +1,5 @@
-"""Multi-launch streaming stress on two GPUs (one process, peer access).
+"""Multi-launch streaming stress: producer and consumer on two GPUs (one
+process, peer access), or on one GPU with a system-scope ring and two streams.
 
 Many put / consume launch pairs are queued back to back on two streams (no
 host synchronisation between launches), as the benchmark does, with the ring
@@ -12,11 +13,12 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
-pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+pytestmark = [pytest.mark.gpu]
+CROSS = pytest.mark.parametrize("cross", [False, pytest.param(True, marks=pytest.mark.multigpu)])
 
 import synth  # noqa: E402
 from oracle.ring import Layout, Sim, Msg, run, decode_header  # noqa: E402
-from gpu_util import upload, msg_tensor, views_host, expected_header  # noqa: E402
+from gpu_util import upload, msg_tensor, views_host, expected_header, devices  # noqa: E402
 
 
 def _need(n):
@@ -26,7 +28,7 @@ def _need(n):
 
 @pytest.fixture(scope="module")
 def R():
-    _need(2)
+    _need(1)
     from paper_2601_20655_b200 import ring
     ring.ring_set_timeout_ns(5_000_000_000)
     return ring
@@ -44,8 +46,10 @@ def _first_mismatch(views, sim, stream):
     return None
 
 
+@CROSS
 @pytest.mark.parametrize("copy", [False, True])
-def test_pipelined_launches_p2p_c3(R, copy):
+def test_pipelined_launches_p2p_c3(R, copy, cross):
+    prod, cons = devices(2, cross)
     L = Layout(64 << 20, 64)
     m, steps = 32, 24
     base = synth.wan_stream(synth.SEED_BASE + 3, 0, 2 * m)            # two distinct source sets
@@ -53,16 +57,16 @@ def test_pipelined_launches_p2p_c3(R, copy):
     msgs = [Msg(x.length, x.payload.tobytes(), x.uid, x.accepted_at, x.app_id, x.stage) for x in stream]
     sim = Sim(L, {0: msgs}, mpsc=False, block=True, depth=1, check=False)
     run(sim, policy="drain")
-    ring = R.ring_create(1, L.R, L.N, 1, 0)
-    peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
+    ring = R.ring_create(cons, L.R, L.N, 1, 0)
+    peer, mh = R.ring_attach_peer(R.ring_export(ring), prod, 0)
     R.ring_bind_mirror(ring, 0, mh)
-    buf, srcs = upload(base, "cuda:0")
-    d_msgs = [msg_tensor(base[s * m:(s + 1) * m], srcs[s * m:(s + 1) * m], "cuda:0") for s in range(2)]
-    sts = [torch.full((m,), 10, dtype=torch.int32, device="cuda:0") for _ in range(steps)]
-    vws = [torch.zeros(m * 128, dtype=torch.uint8, device="cuda:1") for _ in range(steps)]
+    buf, srcs = upload(base, f"cuda:{prod}")
+    d_msgs = [msg_tensor(base[s * m:(s + 1) * m], srcs[s * m:(s + 1) * m], f"cuda:{prod}") for s in range(2)]
+    sts = [torch.full((m,), 10, dtype=torch.int32, device=f"cuda:{prod}") for _ in range(steps)]
+    vws = [torch.zeros(m * 128, dtype=torch.uint8, device=f"cuda:{cons}") for _ in range(steps)]
     cap = 4194304
-    dsts = [torch.zeros(m * cap, dtype=torch.uint8, device="cuda:1") for _ in range(2)] if copy else None
-    sc, sp = torch.cuda.Stream(1), torch.cuda.Stream(0)
+    dsts = [torch.zeros(m * cap, dtype=torch.uint8, device=f"cuda:{cons}") for _ in range(2)] if copy else None
+    sc, sp = torch.cuda.Stream(cons), torch.cuda.Stream(prod)
     for s in range(steps):
         if copy:
             R.ring_consume(ring, m, vws[s], dsts[s % 2], cap, 0, sc)
@@ -71,8 +75,8 @@ def test_pipelined_launches_p2p_c3(R, copy):
         else:
             R.ring_consume(ring, m, vws[s], None, 0, 0, sc)
         R.ring_put_batch(peer, d_msgs[s % 2], m, 0, sts[s], sp)
-    torch.cuda.synchronize(0)
-    torch.cuda.synchronize(1)
+    torch.cuda.synchronize(prod)
+    torch.cuda.synchronize(cons)
     assert all((st == 0).all().item() for st in sts), [np.unique(st.cpu().numpy()).tolist() for st in sts]
     views = np.concatenate([views_host(v) for v in vws])
     mm = _first_mismatch(views, sim, stream)
@@ -89,30 +93,32 @@ def test_pipelined_launches_p2p_c3(R, copy):
     R.ring_destroy(ring)
 
 
-def test_pipelined_launches_small_ring_many_laps(R):
+@CROSS
+def test_pipelined_launches_small_ring_many_laps(R, cross):
     """C1-sized ring (32 KiB, 8 slots), 100 launches x 20 messages of U[1,4096] B:
     hundreds of laps, a PAD at nearly every wrap, the producer waiting for
     credit inside every launch."""
+    prod, cons = devices(2, cross)
     L = Layout(32768, 8)
     m, steps = 20, 100
     stream = synth.random_stream(synth.SEED_BASE + 11, 0, m * steps, 1, 4096)
     msgs = [Msg(x.length, x.payload.tobytes(), x.uid, x.accepted_at, x.app_id, x.stage) for x in stream]
     sim = Sim(L, {0: msgs}, mpsc=False, block=True, depth=1, check=False)
     run(sim, policy="drain")
-    ring = R.ring_create(1, L.R, L.N, 1, 0)
-    peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
+    ring = R.ring_create(cons, L.R, L.N, 1, 0)
+    peer, mh = R.ring_attach_peer(R.ring_export(ring), prod, 0)
     R.ring_bind_mirror(ring, 0, mh)
-    buf, srcs = upload(stream, "cuda:0")
-    d_msgs = msg_tensor(stream, srcs, "cuda:0")
-    sts = torch.full((m * steps,), 10, dtype=torch.int32, device="cuda:0")
-    vws = torch.zeros(m * steps * 128, dtype=torch.uint8, device="cuda:1")
-    dst = torch.zeros(m * steps * 4096, dtype=torch.uint8, device="cuda:1")
-    sc, sp = torch.cuda.Stream(1), torch.cuda.Stream(0)
+    buf, srcs = upload(stream, f"cuda:{prod}")
+    d_msgs = msg_tensor(stream, srcs, f"cuda:{prod}")
+    sts = torch.full((m * steps,), 10, dtype=torch.int32, device=f"cuda:{prod}")
+    vws = torch.zeros(m * steps * 128, dtype=torch.uint8, device=f"cuda:{cons}")
+    dst = torch.zeros(m * steps * 4096, dtype=torch.uint8, device=f"cuda:{cons}")
+    sc, sp = torch.cuda.Stream(cons), torch.cuda.Stream(prod)
     for s in range(steps):
         R.ring_consume(ring, m, vws[s * m * 128:(s + 1) * m * 128], dst[s * m * 4096:(s + 1) * m * 4096], 4096, 0, sc)
         R.ring_put_batch(peer, d_msgs[s * m * 48:(s + 1) * m * 48], m, 0, sts[s * m:(s + 1) * m], sp)
-    torch.cuda.synchronize(0)
-    torch.cuda.synchronize(1)
+    torch.cuda.synchronize(prod)
+    torch.cuda.synchronize(cons)
     assert (sts == 0).all().item(), np.unique(sts.cpu().numpy()).tolist()
     views = views_host(vws)
     mm = _first_mismatch(views, sim, stream)
