@@ -25,8 +25,7 @@ cudaError_t launch_clock_publish(unsigned long long* mapped_host, unsigned long 
 }
 
 cudaError_t preload_clock() {
-  cudaFuncAttributes fa;
-  return cudaFuncGetAttributes(&fa, clock_publish_kernel);
+  return preload_kernel(clock_publish_kernel);
 }
 
 }  // namespace b200ring

@@ -185,9 +185,8 @@ __global__ void __launch_bounds__(32) set_consume_kernel(const SetArgs a) {
 }
 
 cudaError_t preload_fanin() {
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, set_consume_kernel<true>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, set_consume_kernel<false>);
+  cudaError_t e = preload_kernel(set_consume_kernel<true>);
+  if (e == cudaSuccess) e = preload_kernel(set_consume_kernel<false>);
   return e;
 }
 

@@ -351,11 +351,10 @@ __global__ void release_kernel(const ReleaseArgs a) {
 }
 
 cudaError_t preload_get() {   // see preload_put (put.cu)
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, get_kernel<true>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, get_kernel<false>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, release_kernel<true>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, release_kernel<false>);
+  cudaError_t e = preload_kernel(get_kernel<true>);
+  if (e == cudaSuccess) e = preload_kernel(get_kernel<false>);
+  if (e == cudaSuccess) e = preload_kernel(release_kernel<true>);
+  if (e == cudaSuccess) e = preload_kernel(release_kernel<false>);
   return e;
 }
 

@@ -403,7 +403,11 @@ ring_status_t ring_attach_peer(const ring_handle_t* h, int producer_device, uint
   p->desc.rc = ((b.flags & RING_CREATE_RESERVE_COMMIT) && p->desc.mpsc && !p->desc.ft) ? 1u : 0u;
   p->desc.producer_id = producer_id;
   p->desc.has_mirror = 0;
-  p->desc.sys = (same_process && producer_device == b.device) ? 0u : 1u;
+  // Scope follows the ring: a ring created without RING_CREATE_LOCAL is a
+  // system-scope ring for every producer, including one on its own GPU (the
+  // lock, tail and slot words must be accessed with one scope by all of them:
+  // a .gpu atomic next to a peer's .sys atomic is not morally strong).
+  p->desc.sys = (b.flags & RING_CREATE_LOCAL) ? 0u : 1u;
   CUDA_TRY(cudaMalloc(&p->desc_dev, sizeof(DestDesc)));
   CUDA_TRY(cudaMemcpy(p->desc_dev, &p->desc, sizeof(DestDesc), cudaMemcpyHostToDevice));
   ring_status_t s = crc_table_dev(producer_device, &p->crc);
@@ -617,7 +621,11 @@ ring_status_t ring_peer_trace(ring_peer_t p, uint64_t* host_out, uint32_t n) {
 // warp of the grid copies.  NVLink: ~32 SMs of 16-B stores saturate one peer
 // link (profiles/r01_probe*.txt: 678-695 GB/s from 32 CTAs up); HBM->HBM
 // (same-GPU ring): one CTA per SM.
-static void default_grid(int device, bool sys, uint32_t* ctas, uint32_t* threads, uint32_t* chunk) {
+// `remote`: the destination ring sits on another GPU (NVLink); a system-scope
+// ring on the producer's own GPU takes the HBM grid (its CTAs must also fit next
+// to the consumer's: 512-thread put CTAs do not fit beside a copy-out get CTA).
+static void default_grid(int device, bool remote, uint32_t* ctas, uint32_t* threads, uint32_t* chunk) {
+  const bool sys = remote;
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
   if (!*ctas) *ctas = sys ? 33u : (uint32_t)nsm;
@@ -667,7 +675,7 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   a.flags = flags;
   uint32_t ctas = p->copy_ctas, thr = p->threads, chunk = p->chunk;
   DevGuard g(p->device);
-  default_grid(p->device, p->desc.sys, &ctas, &thr, &chunk);
+  default_grid(p->device, p->device != p->ring_device, &ctas, &thr, &chunk);
   a.copy_mode = p->copy_mode;
   // engine stages live in shared memory: the largest power of two that fits
   while (a.copy_mode == 1 && chunk > 4096 && (uint64_t)chunk * kEngineStages > kEngineSmem) chunk >>= 1;
@@ -939,11 +947,11 @@ ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, 
   a.timeout_ns = g_timeout_ns;
   a.n = n;
   a.flags = flags;
-  bool sys = false;
-  for (auto* p : r->dests) sys = sys || p->desc.sys;
+  bool remote = false;
+  for (auto* p : r->dests) remote = remote || p->ring_device != r->device;
   uint32_t ctas = r->copy_ctas, thr = r->threads, chunk = r->chunk;
   DevGuard g(r->device);
-  default_grid(r->device, sys, &ctas, &thr, &chunk);
+  default_grid(r->device, remote, &ctas, &thr, &chunk);
   a.chunk = chunk;
   a.launch = r->launches;
   CUDA_TRY(launch_put(a, ctas, thr, as_stream(stream)));

@@ -210,6 +210,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
       // after our own previous items (and their Unlock) are published.
       while (!D.rc && ld_acquire_gpu32(&S->pub_seq) != L.items)   // RC: the leader unlocks itself
         if (globaltimer() - t_start > a.timeout_ns) { o.status = RING_ETIMEDOUT; break; }
+      if (a.trace) { a.trace[1900] = globaltimer(); a.trace[1901] = L.items; a.trace[1902] = ld_acquire_gpu32(&S->pub_seq); }
       if (o.status == RING_OK && D.rc) {
         // reserve-then-commit: a lock word with an acquisition count, taken
         // over from a lost holder after TL (the lock is held only for claims)
@@ -221,6 +222,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         while (true) {
           const uint64_t old = D.sys ? cas_acquire<true>(lock_w(D), 0ull, me) : cas_acquire<false>(lock_w(D), 0ull, me);
           if (old == 0) { locked = true; break; }
+          if (a.trace) a.trace[1903] = old;
           if (globaltimer() - t_start > a.timeout_ns) { o.status = RING_ETIMEDOUT; break; }
         }
       }
@@ -236,6 +238,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
       } else if (locked) {
         // Step 2: read the tail (ordered after the acquiring CAS).
         P = D.sys ? ld_relaxed<true>(tail_w(D)) : ld_relaxed<false>(tail_w(D));
+        if (a.trace) { a.trace[1904] = globaltimer(); a.trace[1905] = P; }
         // Step 4 (R6, before the space check): a busy slot at P_seq with the
         // size ring not full means a lost sender committed WB+WL but not UH
         // (Case 7): advance the header past it first.  The head is read
@@ -253,6 +256,13 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
       }
     }
     bool defer = false;
+    // a PAD planned for this message is withdrawn if the message is deferred
+    // (below): PAD and message are placed under one lock hold, as the
+    // sender's steps 1-8 place them (R3), so no other sender's entry can land
+    // between them
+    const uint32_t items_in = L.items;
+    const uint64_t P_in = P;
+    const auto last_pad_in = last_pad;
     // Step 3: space check (R4), PAD entry at the wrap (R3), credit wait (R12).
     if (o.status == RING_OK) {
       while (true) {
@@ -319,8 +329,10 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
           continue;
         }
         if (l > 0) {
-          // Hand what is decided (and any PAD just planned) to the copy
-          // warps and the publisher (and release the lock) before waiting.
+          // Hand what is decided to the copy warps and the publisher (and
+          // release the lock) before waiting; this message, with its PAD, is
+          // placed again in the next round.
+          if (!D.rc && L.items != items_in) { L.items = items_in; P = P_in; last_pad = last_pad_in; }
           defer = true;
           break;
         }
@@ -328,6 +340,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         // consumer may have to free it for this message to fit (R3).
         st_release<false>(&S->planned, make_planned(L.items, L.units));
         if (!t_start) t_start = globaltimer();
+        if (a.trace) { a.trace[1906] = globaltimer(); a.trace[1907] = P; a.trace[1908] = H2; a.trace[1909] = f; a.trace[1910]++; }
         uint64_t H3 = H2;
         while (H3 == H2) {
           if (globaltimer() - t_start > a.timeout_ns) break;
@@ -1140,6 +1153,7 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
   __shared__ uint32_t s_crc[kCrcTableWords];
   __shared__ CopyShared cs;
   const int lane = threadIdx.x & 31;
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 120) a.trace[1920 + blockIdx.x] = globaltimer();
   if (threadIdx.x == 0) {
     cs.pl = 0;
     cs.owner = 0;
@@ -1187,10 +1201,9 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
 // spinning for data would then block the producer's first launch until it
 // times out; so every kernel is loaded when a device is first used.
 cudaError_t preload_put() {
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, put_kernel<0>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, put_kernel<1>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, put_kernel<2>);
+  cudaError_t e = preload_kernel(put_kernel<0>);
+  if (e == cudaSuccess) e = preload_kernel(put_kernel<1>);
+  if (e == cudaSuccess) e = preload_kernel(put_kernel<2>);
   if (e == cudaSuccess)   // TMA engine stages (up to kEngineStages x 48 KiB)
     e = cudaFuncSetAttribute(put_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEngineSmem);
   return e;

@@ -223,6 +223,23 @@ struct ReleaseArgs {
 cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s);
 cudaError_t launch_get(const GetArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s);
 cudaError_t launch_release(const ReleaseArgs& a, cudaStream_t s);
+// Load a kernel on the current device now and give it the ring's shared-memory
+// carveout.  Lazy loading: a module loaded at first launch waits for the
+// kernels already running, and a consumer may be spinning for that launch's
+// data.  Carveout: on B200 a CTA is only placed on an SM whose L1/shared split
+// matches its kernel's, and without a preference every kernel gets the
+// smallest split its static shared memory fits -- a 148-CTA put (11 KB static)
+// then leaves no SM on which a 1-CTA get (4 KB) can start, and a put spinning
+// for the get's credit only ends by timing out (profiles/r02_sched_carveout.txt).
+// Every ring kernel therefore asks for the same split (all shared).
+template <class K>
+cudaError_t preload_kernel(K* k) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, k);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+  return e;
+}
 cudaError_t preload_put();
 cudaError_t preload_get();
 cudaError_t preload_clock();

@@ -56,9 +56,8 @@ __global__ void __launch_bounds__(256) stage_scale_put_kernel(const StageArgs a)
 }
 
 cudaError_t preload_stage() {
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, stage_scale_put_kernel<true>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, stage_scale_put_kernel<false>);
+  cudaError_t e = preload_kernel(stage_scale_put_kernel<true>);
+  if (e == cudaSuccess) e = preload_kernel(stage_scale_put_kernel<false>);
   return e;
 }
 

@@ -39,6 +39,8 @@ def lib():
         L.synth_fill.restype = C.c_int
         L.synth_verify.argtypes = [P, P, P, P, U32, U64, P, P]
         L.synth_verify.restype = C.c_int
+        L.synth_verify_views.argtypes = [P, U32, U64, P, P, P, U64, U64, P, P, P]
+        L.synth_verify_views.restype = C.c_int
         L.synth_word.argtypes = [U64, U32, U64, U64]
         L.synth_word.restype = U64
         _lib = L
@@ -90,6 +92,33 @@ def verify(ptrs, lens, chans, seqs, seed: int, stream=None):
         raise RuntimeError(f"synth_verify: cudaError {st}")
     bad._keep = (p, l, c, q)
     return bad
+
+
+def verify_views(views, n: int, data_base: int, seed: int, chans=None, seqs=None, lut=None, lut_stride: int = 0,
+                 stream=None):
+    """verify() of the payloads that n view records (ring_view_t, 128 B each, a
+    device uint8 tensor) point at inside a ring whose buffer region starts at
+    device address data_base.  Keys: the header's (producer_id, seq) unless
+    chans (int32) / seqs (int64) device tensors are given; lut (int64 device
+    tensor) maps (producer_id, seq) to the generator's seq.  Launches only this
+    library's kernels (no torch kernel, no host synchronisation)."""
+    import torch
+    dev = views.device
+    for t in (chans, seqs, lut):
+        assert t is None or (t.device == dev and t.is_contiguous())
+    assert chans is None or chans.dtype == torch.int32
+    assert seqs is None or seqs.dtype == torch.int64
+    assert lut is None or lut.dtype == torch.int64
+    bad = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    work = torch.empty(max(n, 1) * 4, dtype=torch.int64, device=dev)
+    ptr = (lambda t: t.data_ptr() if t is not None else None)
+    with torch.cuda.device(dev):
+        st = lib().synth_verify_views(views.data_ptr(), n, data_base, ptr(chans), ptr(seqs), ptr(lut), lut_stride,
+                                      seed & (2**64 - 1), work.data_ptr(), bad.data_ptr(), _stream(stream))
+    if st:
+        raise RuntimeError(f"synth_verify_views: cudaError {st}")
+    bad._keep = (views, chans, seqs, lut, work)
+    return bad[:n]
 
 
 def word(seed: int, channel: int, seq: int, i: int) -> int:

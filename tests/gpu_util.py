@@ -132,17 +132,7 @@ def verify_views(ring, vt: torch.Tensor, n: int, seed: int, chans=None, seqs=Non
     device tensor of first-bad offsets (-1 = ok)."""
     base = R.ring_get_info(ring).data
     s = stream if stream is not None else torch.cuda.current_stream(vt.device)
-    with torch.cuda.device(vt.device), torch.cuda.stream(s):
-        raw = vt[: n * 128]
-        q = raw.view(torch.int64).view(n, 16)
-        w = raw.view(torch.int32).view(n, 32)
-        ptr = q[:, 0] + base
-        ln = q[:, 1]
-        ch = w[:, 27] if chans is None else chans
-        sq = w[:, 28].to(torch.int64) if seqs is None else seqs
-        if lut is not None:
-            sq = lut[ch.to(torch.int64) * lut_stride + sq]
-        return SD.verify(ptr, ln, ch, sq, seed, s)
+    return SD.verify_views(vt, n, base, seed, chans, seqs, lut, lut_stride, s)
 
 
 def replay_mpsc(L, progs, order, check=True):

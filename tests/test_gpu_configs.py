@@ -387,7 +387,7 @@ def test_c5b_epoch_flip(R, cross):
         for name, vt, ring, ridx in (("A", vA, ringA, 0), ("B", vB, ringB, 1)):
             v = views_host(vt)
             hd = [decode_header(bytes(x["header"])) for x in v]
-            assert all(int(x["status"]) == 0 for x in v), name
+            assert all(int(x["status"]) == 0 for x in v), (name, [int(x["status"]) for x in v])
             ids = [uid_of[h["uid"]] for h in hd]
             progs = {}
             for p in range(3):

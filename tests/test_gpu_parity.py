@@ -427,7 +427,7 @@ def test_p2p_c3_wan_tensors(R, copy_mode, cross):
     stream = synth.wan_stream(synth.SEED_BASE + 3, 0, 48)
     sim = oracle_spsc(L, to_oracle_msgs(stream))
     v, pl, st, img = _p2p_stream(R, L, stream, prod, cons, 4194304, copy_mode=copy_mode)
-    assert st == [0] * 48
+    assert st == [0] * 48, (st, [int(x["status"]) for x in v])
     check_views_against_oracle(v, sim, 0, stream)
     assert pl == [m.payload.tobytes() for m in stream]
 
