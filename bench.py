@@ -173,6 +173,8 @@ def bench_c2(args):
     R.ring_bind_mirror(ring, 0, mh)
     if args.ctas or args.threads or args.copy_mode:
         R.ring_peer_config(peer, args.ctas, args.threads, args.copy_mode)
+    engine = bool(args.engine) and not args.copy_mode
+    put_flags = R.RING_ASYNC if engine else 0
     stride = (plen + 255) // 256 * 256
     src = torch.empty(sets * m * stride, dtype=torch.uint8, device="cuda")
     for k in range(sets * m):
@@ -193,6 +195,23 @@ def bench_c2(args):
     # With --no-overlap, put(s+1) waits for consume(s) to finish (event).
     sp, sc = torch.cuda.Stream(), torch.cuda.Stream()
     stream = sp
+    def sync(limit_s: float = 60.0):
+        # never torch.cuda.synchronize() while the engine runs: it waits for the
+        # resident engine kernel, which only exits when stopped.  A stream that
+        # does not finish within limit_s ends the bench with a diagnosis
+        # (every device spin has its own timeout, so this means a kernel that
+        # cannot be scheduled).
+        t0 = time.time()
+        for s_ in (sp, sc, torch.cuda.current_stream()):
+            while not s_.query():
+                if time.time() - t0 > limit_s:
+                    log(f"C2: stream {s_} stuck; engine {R.ring_peer_engine_state(peer) if engine else None}; "
+                        f"sp={sp.query()} sc={sc.query()} main={torch.cuda.current_stream().query()}")
+                    os._exit(3)
+                time.sleep(0.0002)
+
+    if engine:
+        R.ring_peer_engine_start(peer, sp)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(min(args.steps, 64))]
     consumed = [torch.cuda.Event()]           # holder: events recorded in a graph capture stay in it
     consumed[0].record(sc)
@@ -208,7 +227,7 @@ def bench_c2(args):
             before_put()
         if timed is not None:
             timed[0].record(sp)
-        R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
+        R.ring_put_batch(peer, d_msgs[i % sets], m, put_flags, status, sp)
         if timed is not None:
             timed[1].record(sp)
             timed[2].record(sc)
@@ -218,9 +237,13 @@ def bench_c2(args):
         if not capturing[0]:
             consumed[0].record(sc)
 
+    log(f"C2: engine={engine}, warm-up")
     for i in range(args.warmup):
         step(i)
-    torch.cuda.synchronize()
+    if engine:
+        R.ring_peer_engine_wait(peer, sp)
+    sync()
+    log("C2: warm-up done")
     assert (status == 0).all().item(), "put failed in warm-up"
     assert (R.parse_views(views.cpu().numpy())["status"] == 0).all(), "consume failed in warm-up"
 
@@ -228,7 +251,9 @@ def bench_c2(args):
     n_ev = min(len(ev), 64)
     for i in range(n_ev):
         step(i, ev[i])
-    torch.cuda.synchronize()
+    if engine:
+        R.ring_peer_engine_wait(peer, sp)
+    sync()
     put_ms = [a.elapsed_time(b) for a, b, c, d in ev[:n_ev]]
     get_ms = [c.elapsed_time(d) for a, b, c, d in ev[:n_ev]]
 
@@ -254,14 +279,15 @@ def bench_c2(args):
         consumed[0].record(sc)
         for _ in range(2):
             graph.replay()
-        torch.cuda.synchronize()
+        sync()
         assert (status == 0).all().item(), "put failed in graph warm-up"
     steps = (args.steps + G - 1) // G * G if graph is not None else args.steps
+    log("C2: timed region")
     clk = Clocks(dev)
     clk.start()
     l0 = R.ring_launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    sync()
     main = torch.cuda.current_stream()
     t_start.record(main)
     if graph is not None:
@@ -272,10 +298,12 @@ def bench_c2(args):
         sc.wait_stream(main)
         for i in range(steps):
             step(args.warmup + i)
+        if engine:
+            R.ring_peer_engine_wait(peer, sp)
         main.wait_stream(sp)
         main.wait_stream(sc)
     t_end.record(main)
-    torch.cuda.synchronize()
+    sync()
     launches = (2 * steps) if graph is not None else R.ring_launch_count() - l0
     clocks = clk.stop()
     ms = t_start.elapsed_time(t_end)
@@ -291,7 +319,7 @@ def bench_c2(args):
     for i in range(lat_steps):
         R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
         R.ring_consume(ring, m, lviews[i], None, 0, 0, sc)
-    torch.cuda.synchronize()
+    sync()
     lat_all = []
     for lv in lviews:
         vv = R.parse_views(lv.cpu().numpy())
@@ -304,7 +332,9 @@ def bench_c2(args):
     value = payload / (ms / 1e3) / 1e9
     f = R.ring_footprint(plen)
     put_bytes = m * (plen + f)                 # read s, write f per message
-    put_avg_ms = statistics.mean(put_ms)
+    # engine: one resident put grid; its time per batch in the stream IS the step
+    # (the events around a doorbell would only time the doorbell)
+    put_avg_ms = (ms / args.steps) if engine else statistics.mean(put_ms)
     peaks, src_kind = load_peaks()
     achieved = put_bytes / (put_avg_ms / 1e3) / 1e9
 
@@ -325,14 +355,14 @@ def bench_c2(args):
 
     for i in range(2):
         e2e_step()
-    torch.cuda.synchronize()
+    sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(e_steps):
         e2e_step()
     sp.wait_stream(sc)
     e1.record(stream)
-    torch.cuda.synchronize()
+    sync()
     e2e = m * plen * e_steps / (e0.elapsed_time(e1) / 1e3) / 1e9
 
     # secondary line: copy-out consume (the consumer copies every payload out of
@@ -342,7 +372,7 @@ def bench_c2(args):
     for i in range(3):
         R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
         R.ring_consume(ring, m, views, dst, plen, 0, sc)
-    torch.cuda.synchronize()
+    sync()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0.record(main)
     sp.wait_stream(main)
@@ -353,7 +383,7 @@ def bench_c2(args):
     main.wait_stream(sp)
     main.wait_stream(sc)
     c1.record(main)
-    torch.cuda.synchronize()
+    sync()
     co_ms = c0.elapsed_time(c1)
     co_ok = bool((status == 0).all().item()) and bool((R.parse_views(views.cpu().numpy())["status"] == 0).all())
     copy_out = {"value": round(m * plen * co_steps / (co_ms / 1e3) / 1e9, 2), "unit": UNIT,
@@ -362,6 +392,9 @@ def bench_c2(args):
                 "what": "same stream with ring_consume copying each payload out (copy-out mode, SURVEY.md d-3)"}
     del dst
 
+    if engine:
+        R.ring_peer_engine_stop(peer, sp)
+        sync()
     cpu = cpu_baseline([plen] * 16, Rb, N, args.cpu_budget)
     R.ring_detach(peer)
     R.ring_destroy(ring)
@@ -373,7 +406,8 @@ def bench_c2(args):
                                "(R=64 MiB), 1,048,512-B payloads (footprint 1 MiB), put batch -> consume batch",
                    "R_bytes": Rb, "n_slots": N, "msgs_per_step": m, "payload_bytes": plen,
                    "l2": "inputs larger than L2 (4 x 64 MiB rotating source sets + 64 MiB ring)",
-                   "consume_mode": "view (zero copy)", "parallelism": "replicas only (1 ring)",
+                   "consume_mode": "view (zero copy)",
+                   "put": "persistent engine, one async doorbell per batch" if engine else "one put launch per batch", "parallelism": "replicas only (1 ring)",
                    "streams": "put on one stream, consume on another; consume(s) overlaps put(s), "
                               "put(s+1) takes credit as consume(s) releases entries (device-side waits)"},
         "msgs_per_s": round(m * args.steps / (ms / 1e3), 1),
@@ -384,7 +418,9 @@ def bench_c2(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("ncu_put_c2.json"),
                      "traffic_source": "profiles/ncu_put_c2.json (ncu --set full, put_kernel, same config)",
-                     "kernel": "put_kernel", "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src_kind})",
+                     "kernel": "put_kernel<0> (persistent engine: time per batch = step time)" if engine
+                     else "put_kernel<0> (CUDA-event average per launch)",
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src_kind})",
                      "algorithmic_bytes_per_launch": put_bytes},
         "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": m * stride,
                 "d2h_bytes_per_step": m * 128},
@@ -636,9 +672,16 @@ def main():
     ap.add_argument("--lat-iters", type=int, default=560,
                     help="N>1: unloaded-latency round trips per size per rank (>= 1,000 samples pooled at N=2)")
     ap.add_argument("--no-overlap", action="store_true", help="N=1: put(s+1) waits for consume(s)")
+    ap.add_argument("--engine", type=int, default=0,
+                    help="N=1: 1 = persistent put engine (doorbells), 0 = one put launch per step")
     ap.add_argument("--graph", action="store_true",
                     help="N=1: replay a CUDA graph of 16 steps in the timed region (default: eager launches)")
+    ap.add_argument("--watchdog", type=float, default=0.0,
+                    help="seconds: dump every Python stack and exit if the run takes longer (debugging)")
     args = ap.parse_args()
+    if args.watchdog > 0:
+        import faulthandler
+        faulthandler.dump_traceback_later(args.watchdog, exit=True)
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":

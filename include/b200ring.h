@@ -50,13 +50,17 @@ typedef enum {
   RING_EDROPPED = 11,  /* fault-tolerant ring: WL found the size slot taken -- the lock was taken over
                           while this sender was delayed ("WL(X) fails due to the busy bit",
                           PAPER.md:797); the message is dropped, no retransmission */
-  RING_EREJECTED = 12  /* routed put: refused by the route's admission control (fast reject) */
+  RING_EREJECTED = 12, /* routed put: refused by the route's admission control (fast reject) */
+  RING_ECLOSED = 13    /* put engine: the queue was closed (stopped, or idle-closed) before this batch reached it;
+                          nothing of the batch was written -- submit it again */
 } ring_status_t;
 
 /* flags for ring_put* / ring_get* */
 #define RING_BLOCK 0u        /* wait for credit / data (default, R12) */
 #define RING_TRY 1u          /* do not wait: RING_FULL / RING_EMPTY */
 #define RING_NO_TIMESTAMP 2u /* leave t_put / t_visible zero */
+#define RING_ASYNC 4u        /* ring_put_batch to a running put engine: return on the stream as soon as the
+                                batch is queued (see ring_peer_engine_start) */
 
 /* flags for ring_create */
 #define RING_CREATE_DEFAULT 0u
@@ -191,9 +195,46 @@ ring_status_t ring_detach(ring_peer_t peer);
  * `d_status` (device, n words) receives one ring_status_t per message
  * (RING_OK / RING_FULL under RING_TRY / RING_ETIMEDOUT / RING_EMSGSIZE).
  * The payloads must stay valid until the launch completes in stream order.
- * Header seq (R18) = this attachment's running message count. */
+ * Header seq (R18) = this attachment's running message count.
+ * While the attachment's put engine runs (below), the batch goes to the
+ * engine instead of a launch: same steps, same placements and statuses. */
 ring_status_t ring_put_batch(ring_peer_t peer, const ring_msg_t* d_msgs, uint32_t n, uint32_t flags,
                              uint32_t* d_status, void* stream);
+/* Persistent put engine of one attachment: ONE resident put grid (the same
+ * leader / publisher / copy warps as a put launch) that takes batch after
+ * batch from a device queue, so that consecutive batches run back to back
+ * with no launch, ramp-up or drain between them (items and copy work units
+ * are numbered across batches, as in one long launch).
+ *   ring_peer_engine_start: launch the engine (on a stream of its own, after
+ *     the work already queued on `stream`).  RING_EINVAL for fault-tolerant or
+ *     reserve-then-commit rings, the TMA copy mode, or an engine already on.
+ *   ring_put_batch while it runs: a one-thread doorbell kernel on `stream`
+ *     queues the batch (stream order = batch order; at most 64 batches in
+ *     flight).  Without RING_ASYNC the doorbell returns once the batch is
+ *     published (the stream semantics of a put launch); with RING_ASYNC it
+ *     returns at once, and the payloads, descriptors and status words must
+ *     stay untouched until ring_peer_engine_wait / _stop has run on a stream.
+ *     ring_put (host header) and routed / fused puts to the attachment are
+ *     RING_EINVAL while the engine runs.
+ *   ring_peer_engine_wait: the stream waits until every queued batch is published.
+ *   ring_peer_engine_stop: the engine drains the queued batches and exits;
+ *     `stream` waits for its exit; ring_put_batch launches again afterwards.
+ *   Idle close: an engine with nothing in flight and no engine call on its
+ *     attachment for the idle time (max(1 s, ring_set_timeout_ns)) closes its
+ *     queue and exits -- so an engine whose process has died ends by itself,
+ *     and a host call that synchronises the whole device (cudaMalloc may)
+ *     waits at most that long; the next ring_put_batch restarts it.  A batch
+ *     whose doorbell finds the queue closed gets RING_ECLOSED statuses (only
+ *     possible if its stream was held back for longer than the idle time).
+ *   While an engine runs, the library's host calls that would synchronise the
+ *   device synchronise the legacy default stream instead.
+ * Limit: 2^31 items / 2^32 work units per engine session (restart to reset). */
+ring_status_t ring_peer_engine_start(ring_peer_t peer, void* stream);
+ring_status_t ring_peer_engine_wait(ring_peer_t peer, void* stream);
+ring_status_t ring_peer_engine_stop(ring_peer_t peer, void* stream);
+/* Engine counters now (host, synchronous, never waits for a stream): batches
+ * posted, fully planned, fully published, and whether the queue is closed. */
+ring_status_t ring_peer_engine_state(ring_peer_t peer, uint64_t* out4);
 /* Single message convenience form: `d_payload` device pointer, `hdr` host
  * pointer (copied into the launch), one status word. */
 ring_status_t ring_put(ring_peer_t peer, const void* d_payload, uint64_t len, const ring_hdr_t* hdr,

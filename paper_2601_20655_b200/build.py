@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             pass
     tmp = LIB + ".tmp"
     subprocess.run([NVCC, "-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
-                    *objs, "-o", tmp], check=True)
+                    *objs, "-Xlinker", "--no-undefined", "-o", tmp], check=True)
     os.replace(tmp, LIB)
     with open(STAMP, "w") as f:
         f.write(" ".join(_extra()))

@@ -104,6 +104,16 @@ std::vector<uint32_t> build_crc_table() {
   return t;
 }
 uint32_t* g_crc_dev[64] = {};
+// Put engines running per device: a resident engine never exits on its own, so
+// while one runs, host calls that would synchronise the whole device
+// synchronise the legacy default stream instead (quiesce).
+std::atomic<int> g_engines[64];
+cudaError_t quiesce() {
+  int device = -1;
+  cudaGetDevice(&device);
+  if (device >= 0 && device < 64 && g_engines[device].load() > 0) return cudaStreamSynchronize(cudaStreamLegacy);
+  return cudaDeviceSynchronize();
+}
 ring_status_t crc_table_dev(int device, const uint32_t** out) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (device < 0 || device >= 64) return RING_EINVAL;
@@ -147,6 +157,15 @@ constexpr uint32_t kTraceWords = 2048;   // debug timeline of one put launch
 
 }  // namespace
 
+int b200ring::ring_carveout_percent() {
+  static const int pct = [] {
+    const char* e = getenv("B200RING_CARVEOUT");
+    const int v = e ? atoi(e) : 8;
+    return v >= 0 && v <= 100 ? v : 8;
+  }();
+  return pct;
+}
+
 // ---------------------------------------------------------------------------
 struct ring_s {
   int device = 0;
@@ -179,6 +198,14 @@ struct ring_peer_s {
   FaultSpec fault;                           // test-only fault injection (fault-tolerant rings)
   void* stage_ctl = nullptr;                 // grid-coordination block of fused puts (ring_stage.cuh)
   uint32_t launches_stage = 0;
+  // persistent put engine (ring_peer_engine_start)
+  EngineQueue* eq = nullptr;
+  EngineHost* eh = nullptr;                  // pinned, mapped: lease / alive
+  cudaStream_t eng_stream = nullptr;
+  cudaEvent_t eng_exit = nullptr;
+  cudaEvent_t eng_ready = nullptr;
+  bool engine_on = false;
+  uint64_t posted = 0;                       // batches submitted to the engine
 };
 
 struct router_s {
@@ -302,7 +329,7 @@ ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uin
   CUDA_TRY(cudaMemset(r->mirrors_dev, 0, sizeof(uint64_t*) * max_producers));
   CUDA_TRY(cudaMalloc(&r->ctx, sizeof(LaunchCtx)));
   CUDA_TRY(cudaMemset(r->ctx, 0, sizeof(LaunchCtx)));
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(quiesce());
   ring_status_t s = crc_table_dev(device, &r->crc);
   if (s != RING_OK) return s;
   *out = r;
@@ -312,7 +339,7 @@ ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uin
 ring_status_t ring_destroy(ring_t r) {
   if (!r) return RING_EINVAL;
   DevGuard g(r->device);
-  cudaDeviceSynchronize();
+  quiesce();
   for (void* p : r->opened) cudaIpcCloseMemHandle(p);
   cudaFree(r->ctx);
   cudaFree(r->mirrors_dev);
@@ -452,20 +479,26 @@ ring_status_t ring_bind_mirror(ring_t r, uint32_t producer_id, const ring_handle
     mirror = static_cast<uint64_t*>(m);
   }
   DevGuard g(r->device);
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(quiesce());
   uint64_t head = 0;
   CUDA_TRY(cudaMemcpy(&head, r->base + kHeadOff, 8, cudaMemcpyDeviceToHost));
   head |= kMirrorValid;
   CUDA_TRY(cudaMemcpy(mirror, &head, 8, cudaMemcpyDefault));
   CUDA_TRY(cudaMemcpy(r->mirrors_dev + producer_id, &mirror, sizeof mirror, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(quiesce());
   return RING_OK;
 }
 
 ring_status_t ring_detach(ring_peer_t p) {
   if (!p) return RING_EINVAL;
   DevGuard g(p->device);
-  cudaDeviceSynchronize();
+  if (p->engine_on) ring_peer_engine_stop(p, nullptr);
+  quiesce();
+  if (p->eq) cudaFree(p->eq);
+  if (p->eh) cudaFreeHost(p->eh);
+  if (p->eng_exit) cudaEventDestroy(p->eng_exit);
+  if (p->eng_ready) cudaEventDestroy(p->eng_ready);
+  if (p->eng_stream) cudaStreamDestroy(p->eng_stream);
   if (p->ipc_opened) cudaIpcCloseMemHandle(p->ring);
   cudaFree(p->desc_dev);
   cudaFree(p->ctx);
@@ -531,7 +564,7 @@ ring_status_t ring_set_create(const ring_t* rings, uint32_t n, ring_set_t* out) 
 ring_status_t ring_set_destroy(ring_set_t s) {
   if (!s) return RING_EINVAL;
   DevGuard g(s->device);
-  cudaDeviceSynchronize();
+  quiesce();
   cudaFree(s->rings_dev);
   delete s;
   return RING_OK;
@@ -549,12 +582,12 @@ ring_status_t ring_set_consume(ring_set_t s, uint32_t n, ring_view_t* d_views, u
 }
 
 ring_status_t ring_peer_device_view(ring_peer_t p, ring_dev_peer_t* out) {
-  if (!p || !out || p->desc.mpsc) return RING_EINVAL;
+  if (!p || !out || p->desc.mpsc || p->engine_on) return RING_EINVAL;
   DevGuard g(p->device);
   if (!p->stage_ctl) {
     CUDA_TRY(cudaMalloc(&p->stage_ctl, sizeof(stage::StageCtl)));
     CUDA_TRY(cudaMemset(p->stage_ctl, 0, sizeof(stage::StageCtl)));
-    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(quiesce());
   }
   memset(out, 0, sizeof *out);
   out->ring = reinterpret_cast<uint64_t>(p->desc.ring);
@@ -608,7 +641,7 @@ ring_status_t ring_peer_trace(ring_peer_t p, uint64_t* host_out, uint32_t n) {
   if (!p || !host_out) return RING_EINVAL;
   if (!p->trace) return RING_EINVAL;
   DevGuard g(p->device);
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(quiesce());
   // two halves (launch parity): the last launch first, then the one before it
   const uint32_t last = (p->launches + 1) & 1;
   const uint32_t n0 = std::min<uint32_t>(n, kTraceWords), n1 = std::min<uint32_t>(n - n0, kTraceWords);
@@ -655,9 +688,28 @@ static void default_grid(int device, bool remote, uint32_t* ctas, uint32_t* thre
   }
 }
 
+static ring_status_t engine_launch(ring_peer_t p, void* stream);
+
 static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const ring_msg_t* inline_msg, uint32_t n,
                                 uint32_t flags, uint32_t* d_status, void* stream) {
   if (!p || !d_status || n == 0 || (!d_msgs && !inline_msg)) return RING_EINVAL;
+  if (p->engine_on) {
+    // the resident engine takes the batch: one doorbell thread on `stream`
+    if (!d_msgs) return RING_EINVAL;   // the engine reads descriptors from device memory
+    DevGuard g(p->device);
+    p->eh->lease = p->eh->lease + 1;
+    if (p->eh->alive == 0u) {          // it closed itself while idle: a new session
+      ring_status_t s = engine_launch(p, stream);
+      if (s != RING_OK) return s;
+    }
+    CUDA_TRY(launch_engine_doorbell(p->eq, p->posted, d_msgs, d_status, n, flags & ~RING_ASYNC,
+                                    !(flags & RING_ASYNC), g_timeout_ns, as_stream(stream)));
+    p->posted++;
+    p->base += n;
+    g_launches++;
+    return RING_OK;
+  }
+  if (flags & RING_ASYNC) return RING_EINVAL;
   PutArgs a{};
   if (inline_msg) a.inline_msg = *inline_msg;
   a.msgs = d_msgs;
@@ -693,6 +745,114 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   p->launches++;
   p->base += n;
   g_launches++;
+  return RING_OK;
+}
+
+// ---- persistent put engine -----------------------------------------------------
+// Launch an engine session on the attachment's own stream, after the work
+// queued on `stream` (and after the previous session's kernel); later work on
+// `stream` comes after the queue reset, never after the engine.
+static ring_status_t engine_launch(ring_peer_t p, void* stream) {
+  DevGuard g(p->device);
+  if (!p->eq) {
+    CUDA_TRY(cudaMalloc(&p->eq, sizeof(EngineQueue)));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&p->eh), sizeof(EngineHost), cudaHostAllocMapped));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->eng_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->eng_exit, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->eng_ready, cudaEventDisableTiming));
+  }
+  p->eh->lease = p->eh->lease + 1;
+  p->eh->alive = 1u;
+  CUDA_TRY(cudaEventRecord(p->eng_ready, as_stream(stream)));
+  CUDA_TRY(cudaStreamWaitEvent(p->eng_stream, p->eng_ready, 0));
+  CUDA_TRY(cudaMemsetAsync(p->eq, 0, sizeof(EngineQueue), p->eng_stream));
+  CUDA_TRY(cudaEventRecord(p->eng_ready, p->eng_stream));
+  CUDA_TRY(cudaStreamWaitEvent(as_stream(stream), p->eng_ready, 0));
+  EngineHost* eh_dev = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&eh_dev), p->eh, 0));
+  PutArgs a{};
+  a.ctx = p->ctx;
+  a.dests = p->desc_dev;
+  a.dest0 = p->desc;
+  a.n_dests = 1;
+  a.lock_timeout_ns = g_lock_timeout_ns;
+  a.hole_timeout_ns = g_hole_timeout_ns;
+  a.crc_table = p->crc;
+  a.timeout_ns = g_timeout_ns;
+  a.engine = p->eq;
+  a.engine_host = eh_dev;
+  a.engine_idle_ns = std::max<uint64_t>(1000000000ull, g_timeout_ns);
+  if (getenv("B200RING_TRACE")) {
+    if (!p->trace) {
+      CUDA_TRY(cudaMalloc(&p->trace, 2 * kTraceWords * 8));
+      CUDA_TRY(cudaMemset(p->trace, 0, 2 * kTraceWords * 8));
+    }
+    a.trace = p->trace + (p->launches & 1) * kTraceWords;
+    CUDA_TRY(cudaMemsetAsync(a.trace, 0, kTraceWords * 8, p->eng_stream));
+  }
+  uint32_t ctas = p->copy_ctas, thr = p->threads, chunk = p->chunk;
+  if (!ctas && p->device == p->ring_device) {
+    // a resident grid on every SM would leave no SM for kernels with another
+    // shared-memory split (they only start next to CTAs of the same split)
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+    ctas = (uint32_t)std::max(1, nsm - 8);
+  }
+  default_grid(p->device, p->device != p->ring_device, &ctas, &thr, &chunk);
+  a.chunk = chunk;
+  a.launch = p->launches;
+  CUDA_TRY(launch_put(a, ctas, thr, p->eng_stream));
+  CUDA_TRY(cudaEventRecord(p->eng_exit, p->eng_stream));
+  p->launches++;
+  g_launches++;
+  p->posted = 0;
+  return RING_OK;
+}
+
+ring_status_t ring_peer_engine_start(ring_peer_t p, void* stream) {
+  if (!p || p->engine_on || p->desc.ft || p->desc.rc || p->copy_mode != 0) return RING_EINVAL;
+  ring_status_t s = engine_launch(p, stream);
+  if (s != RING_OK) return s;
+  p->engine_on = true;
+  if (p->device >= 0 && p->device < 64) g_engines[p->device]++;
+  return RING_OK;
+}
+
+ring_status_t ring_peer_engine_state(ring_peer_t p, uint64_t* out4) {
+  if (!p || !out4 || !p->eq) return RING_EINVAL;
+  DevGuard g(p->device);
+  cudaStream_t s = nullptr;   // a private non-blocking stream: never waits for the engine or the user's streams
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  uint64_t v[64];
+  cudaError_t e = cudaMemcpyAsync(v, p->eq, sizeof v, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  CUDA_TRY(e);
+  out4[0] = v[0] & ~kEngineClosed;   // posted
+  out4[1] = v[16];                   // planned_batches
+  out4[2] = v[32];                   // done
+  out4[3] = v[0] >> 63;              // closed
+  return RING_OK;
+}
+
+ring_status_t ring_peer_engine_wait(ring_peer_t p, void* stream) {
+  if (!p || !p->engine_on) return RING_EINVAL;
+  DevGuard g(p->device);
+  p->eh->lease = p->eh->lease + 1;
+  CUDA_TRY(launch_engine_wait(p->eq, p->posted, 2 * g_timeout_ns, as_stream(stream)));
+  g_launches++;
+  return RING_OK;
+}
+
+ring_status_t ring_peer_engine_stop(ring_peer_t p, void* stream) {
+  if (!p || !p->engine_on) return RING_EINVAL;
+  DevGuard g(p->device);
+  p->eh->lease = p->eh->lease + 1;
+  CUDA_TRY(launch_engine_stop(p->eq, as_stream(stream)));
+  CUDA_TRY(cudaStreamWaitEvent(as_stream(stream), p->eng_exit, 0));   // the engine has drained and exited
+  g_launches++;
+  p->engine_on = false;
+  if (p->device >= 0 && p->device < 64) g_engines[p->device]--;
   return RING_OK;
 }
 
@@ -783,7 +943,7 @@ ring_status_t ring_read_image(ring_t r, uint64_t* lock, uint64_t* tail, uint64_t
                               uint64_t* slots) {
   if (!r) return RING_EINVAL;
   DevGuard g(r->device);
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(quiesce());
   uint64_t w[4];
   CUDA_TRY(cudaMemcpy(&w[0], r->base + kLockOff, 8, cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemcpy(&w[1], r->base + kTailOff, 8, cudaMemcpyDeviceToHost));
@@ -800,7 +960,7 @@ ring_status_t ring_read_image(ring_t r, uint64_t* lock, uint64_t* tail, uint64_t
 ring_status_t ring_read_data(ring_t r, uint64_t offset, uint64_t len, void* host_dst) {
   if (!r || (len && !host_dst) || offset > r->R || len > r->R - offset) return RING_EINVAL;
   DevGuard g(r->device);
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(quiesce());
   if (len) CUDA_TRY(cudaMemcpy(host_dst, r->base + r->data_off + offset, len, cudaMemcpyDeviceToHost));
   return RING_OK;
 }
@@ -808,9 +968,9 @@ ring_status_t ring_read_data(ring_t r, uint64_t offset, uint64_t len, void* host
 ring_status_t ring_write_data(ring_t r, uint64_t offset, uint64_t len, const void* host_src) {
   if (!r || (len && !host_src) || offset > r->R || len > r->R - offset) return RING_EINVAL;
   DevGuard g(r->device);
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(quiesce());
   if (len) CUDA_TRY(cudaMemcpy(r->base + r->data_off + offset, host_src, len, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(quiesce());
   return RING_OK;
 }
 
@@ -838,7 +998,7 @@ ring_status_t router_create(int device, uint32_t max_routes, router_t* out) {
 ring_status_t router_destroy(router_t r) {
   if (!r) return RING_EINVAL;
   DevGuard g(r->device);
-  cudaDeviceSynchronize();
+  quiesce();
   cudaFree(r->ctx);
   cudaFree(r->dests_dev);
   cudaFree(r->routes_dev);
@@ -929,8 +1089,10 @@ ring_status_t router_size_route(router_t r, uint32_t app_id, uint16_t stage, uin
 
 ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, uint32_t flags, uint32_t* d_status,
                               uint32_t* d_dest, void* stream) {
-  if (!r || !d_msgs || !d_status || n == 0) return RING_EINVAL;
+  if (!r || !d_msgs || !d_status || n == 0 || (flags & RING_ASYNC)) return RING_EINVAL;
   if (r->dests.empty()) return RING_EINVAL;
+  for (auto* p : r->dests)
+    if (p->engine_on) return RING_EINVAL;   // the attachment's state belongs to its engine
   PutArgs a{};
   a.msgs = d_msgs;
   a.status = d_status;

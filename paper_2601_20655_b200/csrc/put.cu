@@ -63,6 +63,7 @@ struct LeaderState {
   bool aborted;
   bool dead;                        // fault injection (reserve-then-commit): the sender is lost
   bool flow_to;                     // plan-ring flow control timed out: plan slots may still be in use
+  uint32_t nrounds;                 // rounds so far (debug timeline of an engine: the last 64 rounds)
   uint64_t me;                      // reserve-then-commit: this round's lock word
 };
 
@@ -148,7 +149,7 @@ __device__ bool rc_lock(const PutArgs& a, const DestDesc& D, uint64_t me, uint64
   }
 }
 
-__device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, LeaderState& L, uint32_t k0,
+__device__ uint32_t leader_place(const PutArgs& a, uint32_t flags, LaunchCtx* ctx, LaunchSet* S, LeaderState& L, uint32_t k0,
                                  uint32_t gmax, GroupSlot* gs, const MsgBrief* brief, const DestDesc* dests) {
   (void)k0;
   // MPSC: the lock taken for the round's first message is kept for the
@@ -302,7 +303,7 @@ __device__ uint32_t leader_place(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S,
         // Not enough credit with the cached head: re-read it once.
         const uint64_t H2 = read_head(D);
         if (H2 != H) { L.heads[d] = H2; continue; }
-        if (a.flags & RING_TRY) { o.status = RING_FULL; break; }   // "release the lock and abort"
+        if (flags & RING_TRY) { o.status = RING_FULL; break; }   // "release the lock and abort"
         if (D.rc && l == 0) {
           // reserve-then-commit: wait for credit WITHOUT the lock (it is only
           // for claims; a holder waiting past TL would be taken over), helping
@@ -696,33 +697,23 @@ __device__ void ft_put(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, uint32_t*
   }
 }
 
-__device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
+// The messages of one batch: a launch's (kernel parameters), or an engine batch's.
+struct BatchRef {
+  const ring_msg_t* msgs;
+  uint32_t* status;
+  uint32_t n, flags;
+};
+
+// One batch of messages (a launch's, or an engine batch's): rounds of up to
+// 32 messages placed by the leader warp, each handed out with one release.
+__device__ __forceinline__ void leader_batch(const PutArgs& a, const BatchRef& B, LaunchCtx* ctx, LaunchSet* S,
+                                             LeaderState& L, GroupSlot* gs, MsgBrief* brief, uint32_t& s_g,
+                                             const DestDesc* s_dests, bool fast) {
   const int lane = threadIdx.x & 31;
-  __shared__ GroupSlot gs[kGroup];
-  __shared__ MsgBrief brief[kGroup];
-  __shared__ uint32_t s_g;
-  __shared__ LeaderState L;
-  __shared__ DestDesc s_dests[kMaxRouterDests];   // destination descriptors, read every message
-  if (a.n_dests == 1) {
-    if (lane == 0) s_dests[0] = a.dest0;
-  } else {
-    for (uint32_t d = lane; d < a.n_dests && d < (uint32_t)kMaxRouterDests; d += 32) s_dests[d] = a.dests[d];
-  }
-  // the fast path (one SPSC destination, no router) reads its state from the kernel parameters
-  const bool fast = !a.routes && a.n_dests == 1 && !a.dest0.mpsc;
-  if (lane == 0) {
-    L.loaded = 0;
-    L.items = 0;
-    L.units = 0;
-    L.aborted = false;
-    L.dead = false;
-    L.flow_to = false;
-  }
-  __syncwarp();
-  for (uint32_t k0 = 0; k0 < a.n;) {
-    const uint32_t gmax = min((uint32_t)kGroup, a.n - k0);
+  for (uint32_t k0 = 0; k0 < B.n;) {
+    const uint32_t gmax = min((uint32_t)kGroup, B.n - k0);
     if ((uint32_t)lane < gmax) {   // stage the round's lengths / routing keys in parallel
-      const ring_msg_t* mp = a.msgs ? a.msgs + k0 + lane : &a.inline_msg;
+      const ring_msg_t* mp = B.msgs ? B.msgs + k0 + lane : &a.inline_msg;
       const uint64_t len = mp->len;
       brief[lane].len = len;
       brief[lane].f = footprint(len);
@@ -745,7 +736,7 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
         while (L.items + 2 * gmax - ld_acquire_gpu32(&S->pub_seq) > (uint32_t)kPlanRing)
           if (globaltimer() > end) { L.aborted = true; L.flow_to = true; break; }
       }
-      const uint32_t rnd = k0 / kGroup;
+      const uint32_t rnd = a.engine ? L.nrounds % 64 : k0 / kGroup;
       if (a.trace && rnd < 64) a.trace[rnd * 4] = globaltimer();
       // the fast path needs destination 0's state and a fresh credit
       if (fast) {
@@ -761,14 +752,14 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     if (L.flow_to) {
       // Plan slots the copy warps / publisher may still read are never
       // overwritten: the remaining messages time out without a plan item.
-      for (uint32_t k = k0 + lane; k < a.n; k += 32) a.status[k] = RING_ETIMEDOUT;
+      for (uint32_t k = k0 + lane; k < B.n; k += 32) B.status[k] = RING_ETIMEDOUT;
       break;
     }
     uint32_t g = 0;
     if (fast && !L.aborted) g = fast_place(a, ctx, L, gmax, gs, brief, a.dest0);
     if (g == 0) {
       const uint32_t it0 = L.items, un0 = L.units;
-      if (lane == 0) s_g = leader_place(a, ctx, S, L, k0, gmax, gs, brief, s_dests);
+      if (lane == 0) s_g = leader_place(a, B.flags, ctx, S, L, k0, gmax, gs, brief, s_dests);
       __syncwarp();
       g = s_g;
       if (L.dead) {              // fault injection: the sender is lost, this round is never planned
@@ -790,7 +781,7 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
       p.first_unit = o.first_unit;
       p.len = 0;
       if (o.status == RING_OK) {
-        const ring_msg_t* mp = a.msgs ? a.msgs + k : &a.inline_msg;
+        const ring_msg_t* mp = B.msgs ? B.msgs + k : &a.inline_msg;
         const DestDesc& D = s_dests[o.dest];
         const uint64_t len = brief[lane].len;
         const uint64_t f = brief[lane].f;
@@ -804,7 +795,9 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
         p.f = f;
         p.seq = o.seq;
         p.epoch = o.epoch;
+        if (a.engine) p.msgp = reinterpret_cast<uint64_t>(mp);
       }
+      if (a.engine) p.statusp = reinterpret_cast<uint64_t>(B.status + k);
       // An arrive counter is reused by item + kPlanRing, planned only once
       // pub_seq has passed the item (flow control); the first kPlanRing items
       // start from the zeroed set, and the speculative first round only ever
@@ -816,10 +809,80 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
     __syncwarp();
     if (lane == 0) {
       st_release<false>(&S->planned, make_planned(L.items, L.units));
-      const uint32_t rnd = k0 / kGroup;
-      if (a.trace && rnd < 64) { a.trace[rnd * 4 + 1] = globaltimer(); a.trace[rnd * 4 + 3] = g; }
+      const uint32_t rnd = a.engine ? L.nrounds++ % 64 : k0 / kGroup;
+      if (a.trace && rnd < 64) {
+        a.trace[rnd * 4 + 1] = globaltimer();
+        a.trace[rnd * 4 + 2] = L.items;
+        a.trace[rnd * 4 + 3] = g;
+      }
     }
     k0 += g;
+  }
+}
+
+
+__device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
+  const int lane = threadIdx.x & 31;
+  __shared__ GroupSlot gs[kGroup];
+  __shared__ MsgBrief brief[kGroup];
+  __shared__ uint32_t s_g;
+  __shared__ LeaderState L;
+  __shared__ DestDesc s_dests[kMaxRouterDests];   // destination descriptors, read every message
+  if (a.n_dests == 1) {
+    if (lane == 0) s_dests[0] = a.dest0;
+  } else {
+    for (uint32_t d = lane; d < a.n_dests && d < (uint32_t)kMaxRouterDests; d += 32) s_dests[d] = a.dests[d];
+  }
+  // the fast path (one SPSC destination, no router) reads its state from the kernel parameters
+  const bool fast = !a.routes && a.n_dests == 1 && !a.dest0.mpsc;
+  if (lane == 0) {
+    L.loaded = 0;
+    L.items = 0;
+    L.units = 0;
+    L.aborted = false;
+    L.dead = false;
+    L.flow_to = false;
+    L.nrounds = 0;
+  }
+  __syncwarp();
+  if (!a.engine) {
+    leader_batch(a, BatchRef{a.msgs, a.status, a.n, a.flags}, ctx, S, L, gs, brief, s_g, s_dests, fast);
+  } else {
+    // Persistent engine: batches from the queue until the host's stop.  Each
+    // batch is independent (a timed-out message aborts the rest of ITS batch).
+    EngineQueue* q = a.engine;
+    uint64_t lease = 0, since = 0;
+    for (uint64_t b = 0;; ++b) {
+      uint32_t go = 0;
+      if (lane == 0) {
+        while (true) {
+          const uint64_t c = ld_acquire<false>(&q->ctl);
+          if ((c & ~kEngineClosed) > b) { go = 1; break; }
+          if (c & kEngineClosed) break;                   // stopped: every posted batch is planned
+          // idle: close the queue once nothing is in flight and the host has
+          // made no call on the attachment for the idle time
+          const uint64_t now = globaltimer();
+          const uint64_t ls = a.engine_host->lease;
+          if (ls != lease || !since || ld_acquire<false>(&q->done) != b) { lease = ls; since = now; }
+          else if (now - since > a.engine_idle_ns && atomicCAS(reinterpret_cast<unsigned long long*>(&q->ctl), c,
+                                                               c | kEngineClosed) == c)
+            break;
+          __nanosleep(256);
+        }
+      }
+      go = __shfl_sync(0xffffffffu, go, 0);
+      if (!go) break;
+      const EngineBatch& eb = q->batch[b % kEngineQueue];
+      const BatchRef B{eb.msgs, eb.status, eb.n, eb.flags};
+      if (lane == 0) { L.aborted = false; L.flow_to = false; }
+      __syncwarp();
+      leader_batch(a, B, ctx, S, L, gs, brief, s_g, s_dests, fast);
+      if (lane == 0) {
+        q->batch[b % kEngineQueue].item_end = L.items;
+        st_release<false>(&q->planned_batches, b + 1);
+      }
+      __syncwarp();
+    }
   }
   if (lane == 0) {
     st_release<false>(&S->planned, make_planned(L.items, L.units) | kPlannedDone);
@@ -828,6 +891,10 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
         a.dests[d].st->chan_seq = L.chans[d];
         if (!a.dests[d].mpsc) a.dests[d].st->tail_cache = L.tails[d];
       }
+  }
+  if (lane == 0 && a.engine) {   // the host restarts a closed engine at its next submission
+    __threadfence_system();
+    a.engine_host->alive = 0u;
   }
 }
 
@@ -840,11 +907,15 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
 __device__ __forceinline__ void write_header(const PutArgs& a, LaunchCtx* ctx, uint32_t j, const uint32_t* crc_tab) {
   const Plan& p = ctx->plan[j % kPlanRing];
   const uint32_t flags = ld_cg32(&p.flags), status = ld_cg32(&p.status), msg = ld_cg32(&p.msg);
-  if (flags & kStatus) a.status[msg] = status;
+  if (flags & kStatus) {
+    if (a.engine) *reinterpret_cast<uint32_t*>(ld_cg64(&p.statusp)) = status;
+    else a.status[msg] = status;
+  }
   if (!(flags & kEntry)) return;
   const DestDesc& D = a.dests[ld_cg32(&p.dest)];
   if ((flags & kStatus) && status == RING_OK) {
-    const ring_msg_t* mp = a.msgs ? a.msgs + msg : &a.inline_msg;
+    const ring_msg_t* mp = a.engine ? reinterpret_cast<const ring_msg_t*>(ld_cg64(&p.msgp))
+                                    : (a.msgs ? a.msgs + msg : &a.inline_msg);
     const uint32_t* uid = reinterpret_cast<const uint32_t*>(mp->hdr.uid);   // (4-B aligned in kernel params)
     const uint4 u0 = make_uint4(uid[0], uid[1], uid[2], uid[3]);
     const uint64_t acc = mp->hdr.accepted_at;
@@ -917,6 +988,16 @@ __device__ void rc_advance(const PutArgs& a, const DestDesc& D, int lane, bool w
   }
 }
 
+// Engine: batches [done, ..) whose every item is below `published` are done;
+// returns the new count (released to the doorbell / wait kernels).
+__device__ __forceinline__ uint64_t engine_advance_done(EngineQueue* q, uint64_t done, uint32_t published) {
+  const uint64_t pb = ld_acquire<false>(&q->planned_batches);
+  const uint64_t d0 = done;
+  while (done < pb && (int32_t)(published - ld_cg32(&q->batch[done % kEngineQueue].item_end)) >= 0) ++done;
+  if (done != d0) st_release<false>(&q->done, done);
+  return done;
+}
+
 // Steps 5-8 (WB header, WL, UH, Unlock), in item order.  As soon as items are
 // planned the lanes write their headers (write_header), off the copy critical
 // path.  For publication lane l caches the plan of item i + l (read once);
@@ -942,6 +1023,7 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
   bool rc_any = false;       // reserve-then-commit: committed entries to see published
   uint32_t rc_last = 0, rc_dest = 0;
   if (a.trace && lane == 0) a.trace[255] = globaltimer();
+  uint64_t bdone = 0;   // engine: batches whose every item is published (lane 0)
   auto flush = [&]() {
     const DestDesc& D = a.dests[pend_dest];
     // acquire for the arrive counters read before, release for the copies, headers and slots
@@ -954,9 +1036,10 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
         if (D.sys) st_release<true>(lock_w(D), 0ull); else st_release<false>(lock_w(D), 0ull);
       }
       st_u32_relaxed_gpu(&S->pub_seq, i);   // ordered by the fence
-      if (a.trace && trace_n < 512) {
-        a.trace[256 + 2 * trace_n] = globaltimer();
-        a.trace[257 + 2 * trace_n] = i;
+      if (a.engine) bdone = engine_advance_done(a.engine, bdone, i);
+      if (a.trace && (trace_n < 512 || a.engine)) {
+        a.trace[256 + 2 * (trace_n % 512)] = globaltimer();
+        a.trace[257 + 2 * (trace_n % 512)] = i;
       }
     }
     trace_n++;
@@ -1008,8 +1091,12 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
     if (run == 0) {
       if (pend) { flush(); continue; }
       const uint64_t t = globaltimer();
+      if (a.engine) {            // batches planned after their items were published
+        if (lane == 0) bdone = engine_advance_done(a.engine, bdone, i);
+        __nanosleep(64);
+      }
       if (!idle_since) idle_since = t;
-      else if (t - idle_since > 2 * a.timeout_ns) break;
+      else if (t - idle_since > 2 * (a.engine ? kForeverNs : a.timeout_ns)) break;
       continue;
     }
     idle_since = 0;
@@ -1083,6 +1170,7 @@ __device__ void put_publisher(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S, co
     if (!full || unlock_now || run < 32 || pend_n >= 96) flush();
   }
   if (pend) flush();
+  if (a.engine && lane == 0) bdone = engine_advance_done(a.engine, bdone, i);
   // reserve-then-commit: the put returns once its entries are published --
   // waited for only here, after every commit of the launch (waiting per run
   // would hold back our later commits that other senders' entries wait on)
@@ -1146,7 +1234,7 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
 // copy warps with 32-B accesses (NVLink destinations).  Separate kernels, so
 // one path's registers never change another's copy loop.
 template <int MODE>
-__global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
+__global__ void __launch_bounds__(512, 1) put_kernel(const __grid_constant__ PutArgs a) {
   LaunchCtx* ctx = a.ctx;
   LaunchSet* S = &ctx->set[a.launch & 1];
   const int warp = threadIdx.x >> 5;
@@ -1193,20 +1281,81 @@ __global__ void __launch_bounds__(512, 1) put_kernel(const PutArgs a) {
   const uint32_t ncopy = blockDim.x - (blockIdx.x == 0 ? 64u : 0u);
   if (warp == (blockIdx.x == 0 ? 2 : 0)) spec_first_round(a, &spec);
   asm volatile("bar.sync 2, %0;" ::"r"(ncopy) : "memory");
-  copy_warp<MODE == 2 ? 2 : 1>(ctx, S, &cs, a.chunk, a.timeout_ns, a.trace, &spec);
+  copy_warp<MODE == 2 ? 2 : 1>(ctx, S, &cs, a.chunk, a.engine ? kForeverNs : a.timeout_ns, a.trace, &spec);
 }
 
 // With CUDA's lazy module loading, the first launch of a kernel loads it, and
 // loading waits for kernels already running on the device.  A consumer kernel
 // spinning for data would then block the producer's first launch until it
 // times out; so every kernel is loaded when a device is first used.
-cudaError_t preload_put() {
-  cudaError_t e = preload_kernel(put_kernel<0>);
-  if (e == cudaSuccess) e = preload_kernel(put_kernel<1>);
-  if (e == cudaSuccess) e = preload_kernel(put_kernel<2>);
-  if (e == cudaSuccess)   // TMA engine stages (up to kEngineStages x 48 KiB)
-    e = cudaFuncSetAttribute(put_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEngineSmem);
-  return e;
+
+// ---- persistent engine: doorbell / stop (one thread, on the submitting stream) ----
+// Batch b goes to slot b % kEngineQueue once the engine is done with batch
+// b - kEngineQueue and batch b - 1 is posted (doorbells on several streams
+// still post in submission order); then `posted` = b + 1 is released.  With
+// `wait`, the kernel returns once the batch is published (stream semantics of
+// a put launch); on a timeout the remaining statuses are left to the engine.
+__global__ void engine_doorbell_kernel(EngineQueue* q, uint64_t b, const ring_msg_t* msgs, uint32_t* status,
+                                       uint32_t n, uint32_t flags, uint32_t wait, uint64_t timeout_ns) {
+  __shared__ uint32_t rejected;
+  if (threadIdx.x == 0) {
+    rejected = 1;
+    const uint64_t t0 = globaltimer();
+    while (true) {
+      const uint64_t c = ld_acquire<false>(&q->ctl);
+      if (c & kEngineClosed) break;                      // closed: the batch is not taken
+      if (c == b && ld_acquire<false>(&q->done) + kEngineQueue > b) {
+        EngineBatch& e = q->batch[b % kEngineQueue];
+        e.msgs = msgs;
+        e.status = status;
+        e.n = n;
+        e.flags = flags;
+        __threadfence();                                 // the slot before the count
+        if (atomicCAS(reinterpret_cast<unsigned long long*>(&q->ctl), b, b + 1) == b) rejected = 0;
+        break;
+      }
+      if (globaltimer() - t0 > timeout_ns) break;
+    }
+    if (!rejected && wait)
+      while (ld_acquire<false>(&q->done) <= b)
+        if (globaltimer() - t0 > 2 * timeout_ns) break;
+  }
+  __syncwarp();
+  if (rejected)
+    for (uint32_t k = threadIdx.x; k < n; k += 32) status[k] = RING_ECLOSED;
+}
+__global__ void engine_stop_kernel(EngineQueue* q) {
+  if (threadIdx.x == 0) {
+    unsigned long long c = ld_acquire<false>(&q->ctl);
+    while (!(c & kEngineClosed)) {
+      const unsigned long long o = atomicCAS(reinterpret_cast<unsigned long long*>(&q->ctl), c, c | kEngineClosed);
+      if (o == c) break;
+      c = o;
+    }
+  }
+}
+__global__ void engine_wait_kernel(EngineQueue* q, uint64_t upto, uint64_t timeout_ns) {
+  if (threadIdx.x != 0) return;
+  const uint64_t t0 = globaltimer();
+  while (true) {
+    const uint64_t c = ld_acquire<false>(&q->ctl), d = ld_acquire<false>(&q->done);
+    if (d >= upto || ((c & kEngineClosed) && d >= (c & ~kEngineClosed))) return;
+    if (globaltimer() - t0 > timeout_ns) return;
+  }
+}
+
+cudaError_t launch_engine_doorbell(EngineQueue* q, uint64_t b, const ring_msg_t* msgs, uint32_t* status, uint32_t n,
+                                   uint32_t flags, bool wait, uint64_t timeout_ns, cudaStream_t s) {
+  engine_doorbell_kernel<<<1, 32, 0, s>>>(q, b, msgs, status, n, flags, wait ? 1u : 0u, timeout_ns);
+  return cudaGetLastError();
+}
+cudaError_t launch_engine_stop(EngineQueue* q, cudaStream_t s) {
+  engine_stop_kernel<<<1, 32, 0, s>>>(q);
+  return cudaGetLastError();
+}
+cudaError_t launch_engine_wait(EngineQueue* q, uint64_t upto, uint64_t timeout_ns, cudaStream_t s) {
+  engine_wait_kernel<<<1, 32, 0, s>>>(q, upto, timeout_ns);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s) {
@@ -1215,6 +1364,18 @@ cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaSt
   else if (a.dest0.sys && !a.routes) put_kernel<2><<<ctas, threads, 0, s>>>(a);
   else put_kernel<0><<<ctas, threads, 0, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t preload_put() {
+  cudaError_t e = preload_kernel(put_kernel<0>);
+  if (e == cudaSuccess) e = preload_kernel(engine_doorbell_kernel);
+  if (e == cudaSuccess) e = preload_kernel(engine_stop_kernel);
+  if (e == cudaSuccess) e = preload_kernel(engine_wait_kernel);
+  if (e == cudaSuccess) e = preload_kernel(put_kernel<1>, (int)cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) e = preload_kernel(put_kernel<2>);
+  if (e == cudaSuccess)   // TMA engine stages (up to kEngineStages x 48 KiB)
+    e = cudaFuncSetAttribute(put_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEngineSmem);
+  return e;
 }
 
 }  // namespace b200ring

@@ -73,7 +73,9 @@ struct alignas(64) Plan {
   uint32_t flags, seq, epoch, _q;   // put: header seq (R18) and epoch of a message entry
   uint64_t f;
   uint64_t start;                   // put: entry offset in the data region (header goes to data + start)
-  uint64_t _p[4];
+  uint64_t msgp;                    // put engine: the message descriptor (header fields) of this item
+  uint64_t statusp;                 // put engine: its status word
+  uint64_t _p[2];
   uint32_t _h[16];
 };
 static_assert(sizeof(Plan) == 192, "Plan layout");
@@ -157,6 +159,47 @@ struct Route {
   uint64_t adm_next;    // device-owned
 };
 
+// Persistent put engine (ring_peer_engine_start): one resident put grid per
+// attachment takes batches from this queue instead of one launch per batch.
+// A doorbell kernel on the submitting stream fills slot b % kEngineQueue and
+// moves `ctl` from b to b + 1 with a CAS (stream order = batch order); the
+// leader plans batch after batch (items and work units numbered across
+// batches, as in one long launch); the publisher releases `done` = b + 1 once
+// every item of batch b is published.  Closing: bit 63 of `ctl` -- set by the
+// stop kernel (the engine drains the batches posted before it and exits) or
+// by the engine itself when it has been idle, with nothing in flight and no
+// host call on the attachment (the host lease), for the idle time: a
+// resident kernel whose process has gone then ends by itself, and a live
+// host restarts it at its next submission (EngineHost::alive).  A doorbell
+// that finds the queue closed writes RING_ECLOSED into its batch's statuses.
+constexpr uint32_t kEngineQueue = 64;
+constexpr uint64_t kEngineClosed = 1ull << 63;
+struct EngineHost {            // pinned, mapped host memory
+  volatile uint64_t lease;     // host: bumped by every engine call of the attachment
+  volatile uint32_t alive;     // host 1 at launch; the engine 0 when it exits
+  uint32_t _p;
+};
+struct EngineBatch {
+  const ring_msg_t* msgs;
+  uint32_t* status;
+  uint32_t n, flags;
+  uint32_t item_end;     // leader: items [.., item_end) hold this batch (valid once planned_batches > b)
+  uint32_t _p;
+};
+struct alignas(128) EngineQueue {
+  uint64_t ctl;               // doorbells: batches posted | kEngineClosed
+  uint64_t _a[15];
+  uint64_t planned_batches;   // leader: batches fully planned
+  uint64_t _b[15];
+  uint64_t done;              // publisher: batches fully published
+  uint64_t _c[15];
+  uint64_t _d[16];
+  EngineBatch batch[kEngineQueue];
+};
+static_assert(offsetof(EngineQueue, planned_batches) == 128 && offsetof(EngineQueue, done) == 256,
+              "EngineQueue layout (ring_peer_engine_state)");
+constexpr uint64_t kForeverNs = 1ull << 60;   // engine copy warps / publisher never give up while idle
+
 struct PutArgs {
   ring_msg_t inline_msg;  // used when msgs == nullptr (ring_put of one message)
   DestDesc dest0;         // dests[0] by value (a peer's only destination: no load before placement)
@@ -180,6 +223,9 @@ struct PutArgs {
   uint64_t lock_timeout_ns;   // TL (fault-tolerant and reserve-then-commit rings)
   uint64_t hole_timeout_ns;   // reserve-then-commit: a reservation this old at the tail is a lost sender's
   FaultSpec fault;            // test-only fault injection
+  EngineQueue* engine;        // persistent put engine: batches come from here (msgs / n / status unused)
+  EngineHost* engine_host;    // its lease / alive words (device address of the mapped host memory)
+  uint64_t engine_idle_ns;    // idle time after which it closes itself
 };
 
 #ifndef B200RING_ENGINE_STAGES
@@ -223,6 +269,10 @@ struct ReleaseArgs {
 cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s);
 cudaError_t launch_get(const GetArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s);
 cudaError_t launch_release(const ReleaseArgs& a, cudaStream_t s);
+cudaError_t launch_engine_doorbell(EngineQueue* q, uint64_t b, const ring_msg_t* msgs, uint32_t* status, uint32_t n,
+                                   uint32_t flags, bool wait, uint64_t timeout_ns, cudaStream_t s);
+cudaError_t launch_engine_stop(EngineQueue* q, cudaStream_t s);
+cudaError_t launch_engine_wait(EngineQueue* q, uint64_t upto, uint64_t timeout_ns, cudaStream_t s);
 // Load a kernel on the current device now and give it the ring's shared-memory
 // carveout.  Lazy loading: a module loaded at first launch waits for the
 // kernels already running, and a consumer may be spinning for that launch's
@@ -231,13 +281,23 @@ cudaError_t launch_release(const ReleaseArgs& a, cudaStream_t s);
 // smallest split its static shared memory fits -- a 148-CTA put (11 KB static)
 // then leaves no SM on which a 1-CTA get (4 KB) can start, and a put spinning
 // for the get's credit only ends by timing out (profiles/r02_sched_carveout.txt).
-// Every ring kernel therefore asks for the same split (all shared).
+// Every ring kernel therefore asks for the same split: 8 % (a 32 KB shared
+// split: room for two put CTAs and a get CTA on one SM), so L1 keeps ~224 KB --
+// the copy loops' outstanding loads are staged in L1, and an all-shared split
+// (28 KB of L1) costs the C2 put ~10-20 %.  Measured (tools/carveout_probe.cu,
+// profiles/r02_carveout_probe.txt): 8 % lets a put grid start next to a
+// copy-out get grid and vice versa; 0-7 % and, oddly, 14 % do not.  The TMA
+// engine (put_kernel<1>, up to 200 KB of stages) takes its own split and starts
+// only on SMs free of other ring kernels.  B200RING_CARVEOUT (percent)
+// overrides the split (experiments).
+int ring_carveout_percent();
 template <class K>
-cudaError_t preload_kernel(K* k) {
+cudaError_t preload_kernel(K* k, int carveout = -1) {
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, k);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             carveout >= 0 ? carveout : ring_carveout_percent());
   return e;
 }
 cudaError_t preload_put();

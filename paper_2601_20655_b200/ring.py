@@ -19,10 +19,10 @@ LIB_PATH = os.path.join(_HERE, "libb200ring.so")
 # ---- status codes / flags (include/b200ring.h) ------------------------------------
 RING_OK, RING_EINVAL, RING_ENOMEM, RING_EMSGSIZE, RING_FULL, RING_EMPTY = 0, 1, 2, 3, 4, 5
 RING_ETIMEDOUT, RING_ECORRUPT, RING_ECUDA, RING_EPEER, RING_EPENDING, RING_EDROPPED = 6, 7, 8, 9, 10, 11
-RING_EREJECTED = 12
+RING_EREJECTED, RING_ECLOSED = 12, 13
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "EMSGSIZE", 4: "FULL", 5: "EMPTY", 6: "ETIMEDOUT",
-                7: "ECORRUPT", 8: "ECUDA", 9: "EPEER", 10: "EPENDING", 11: "EDROPPED", 12: "EREJECTED"}
-RING_BLOCK, RING_TRY, RING_NO_TIMESTAMP = 0, 1, 2
+                7: "ECORRUPT", 8: "ECUDA", 9: "EPEER", 10: "EPENDING", 11: "EDROPPED", 12: "EREJECTED", 13: "ECLOSED"}
+RING_BLOCK, RING_TRY, RING_NO_TIMESTAMP, RING_ASYNC = 0, 1, 2, 4
 RING_CREATE_DEFAULT, RING_CREATE_LOCAL, RING_CREATE_FAULT_TOLERANT, RING_CREATE_RESERVE_COMMIT = 0, 1, 2, 4
 RING_AT_LOCK, RING_AT_GH, RING_AT_WB, RING_AT_WL, RING_AT_UH = 1, 2, 3, 4, 5
 RING_HDR_BYTES, RING_ENTRY_ALIGN = 64, 128
@@ -86,6 +86,10 @@ def _load():
         "ring_put_batch": [P, P, U32, U32, P, P],
         "ring_put": [P, P, U64, C.POINTER(ring_hdr_t), U32, P, P],
         "ring_peer_config": [P, U32, U32, U32],
+        "ring_peer_engine_start": [P, P],
+        "ring_peer_engine_wait": [P, P],
+        "ring_peer_engine_stop": [P, P],
+        "ring_peer_engine_state": [P, C.POINTER(C.c_uint64)],
         "ring_get": [P, U32, P, P, U64, U32, P],
         "ring_release": [P, U32, P],
         "ring_consume": [P, U32, P, P, U64, U32, P],
@@ -212,6 +216,24 @@ def ring_put(peer: int, d_payload, length: int, hdr: ring_hdr_t, flags: int, d_s
 
 def ring_peer_config(peer: int, copy_ctas: int = 0, threads: int = 0, copy_mode: int = 0) -> None:
     _check("ring_peer_config", lib.ring_peer_config(peer, copy_ctas, threads, copy_mode))
+
+
+def ring_peer_engine_start(peer: int, stream=None) -> None:
+    _check("ring_peer_engine_start", lib.ring_peer_engine_start(peer, _stream(stream)))
+
+
+def ring_peer_engine_wait(peer: int, stream=None) -> None:
+    _check("ring_peer_engine_wait", lib.ring_peer_engine_wait(peer, _stream(stream)))
+
+
+def ring_peer_engine_stop(peer: int, stream=None) -> None:
+    _check("ring_peer_engine_stop", lib.ring_peer_engine_stop(peer, _stream(stream)))
+
+
+def ring_peer_engine_state(peer: int) -> dict:
+    out = (C.c_uint64 * 4)()
+    _check("ring_peer_engine_state", lib.ring_peer_engine_state(peer, out))
+    return dict(posted=out[0], planned=out[1], done=out[2], closed=out[3])
 
 
 def ring_peer_submitted(peer: int) -> int:

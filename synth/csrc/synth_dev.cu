@@ -124,13 +124,13 @@ void preload() {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || done[dev]) return;
-  // Same shared-memory carveout as the ring kernels (all shared): a CTA is
+  // Same shared-memory carveout as the ring kernels (8 %: a 32 KB split): a CTA is
   // only placed on an SM whose L1/shared split matches its kernel's, and these
   // kernels must start next to a put that waits for the consumer they serve.
   auto load = [](auto* k) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, k);
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 8);
   };
   load(synth_kernel<false>);
   load(synth_kernel<true>);

@@ -375,6 +375,10 @@ def _p2p_stream(R, L, stream, prod_dev, cons_dev, cap, copy=True, copy_mode=0):
     ring = R.ring_create(cons_dev, L.R, L.N, 1, 0)
     peer, mh = R.ring_attach_peer(R.ring_export(ring), prod_dev, 0)
     R.ring_peer_config(peer, 0, 0, copy_mode)
+    if copy_mode == 1 and prod_dev == cons_dev:
+        # the TMA engine takes its own shared-memory split: it starts only on SMs
+        # free of other ring kernels, so the consumer's copy grid leaves half free
+        R.ring_config(ring, 74, 0)
     R.ring_bind_mirror(ring, 0, mh)
     buf, srcs = upload(stream, f"cuda:{prod_dev}")
     msgs = msg_tensor(stream, srcs, f"cuda:{prod_dev}")
