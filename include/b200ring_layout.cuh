@@ -1,5 +1,6 @@
-// ring_device.cuh — device-side layout, word packing and memory-ordering
-// primitives of the B200 double ring (sm_100a).
+// b200ring_layout.cuh — device-side layout, word packing and memory-ordering
+// primitives of the B200 double ring (sm_100a), shared by the library's
+// kernels and by producer kernels that put from the device (b200ring_device.cuh).
 //
 // Layout ("lock region, fixed-length header
 // with head and tail, buffer region, size region"):
@@ -209,6 +210,10 @@ __device__ __forceinline__ uint32_t crc52(const uint32_t* w, const uint32_t* __r
 // SURVEY.md Q10), one warp per range: lane l takes a contiguous slice, the
 // slice CRCs are combined with crc(A || B) = (crc(A) * x^(8|B|) mod P) ^ crc(B)
 // (GF(2) multiply by a power of x built from the x^(2^n) table `pw`).
+// The GF(2) combine follows the construction of zlib's crc32_combine
+// (multmodp / x2nmodp, zlib 1.2.12+, (C) 1995-2022 Jean-loup Gailly and Mark
+// Adler, zlib license: use permitted with this notice; this is an independent
+// rewrite of that canonical routine, not a copy of its source).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t gf2_mulmod_dev(uint32_t a, uint32_t b) {
   uint32_t p = 0;
@@ -261,5 +266,23 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint8_t* p, uint64_t n, con
   }
   return __shfl_sync(0xffffffffu, c, 0);
 }
+
+
+// Mirror word: head | kMirrorValid once the consumer has bound the mirror.
+constexpr uint64_t kMirrorValid = 1ull << 63;
+
+// Producer-local state of one attachment (one producer -> one ring channel),
+// allocated on the producer GPU and exported to the consumer by CUDA IPC so
+// that the consumer's release can push the head into `mirror_head` (the
+// credit direction of the double ring, R1).
+struct alignas(128) DestState {
+  uint64_t mirror_head;  // written by the consumer (NVLink store); read locally by the leader
+  uint64_t _p0[15];
+  uint64_t tail_cache;   // SPSC: tail after the last planned entry (leader-owned)
+  uint64_t chan_seq;     // next header seq of this channel (R18)
+  uint64_t lock_acq;     // fault-tolerant rings: lock acquisitions by this attachment
+  uint64_t _p1[13];
+};
+static_assert(sizeof(DestState) == 256, "DestState layout");
 
 }  // namespace b200ring

@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libb200ring.so")
 SOURCES = ["host.cu", "put.cu", "get.cu", "clock.cu", "stage.cu", "fanin.cu"]
-HEADERS = ["ring_device.cuh", "ring_internal.h", "ring_copy.cuh", "ring_stage.cuh", os.path.join("..", "..", "include", "b200ring.h")]
+HEADERS = ["ring_internal.h", "ring_copy.cuh"] + [os.path.join("..", "..", "include", h) for h in ("b200ring.h", "b200ring_layout.cuh", "b200ring_device.cuh")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-cudart", "static", "--expt-relaxed-constexpr"]

@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "ring_internal.h"
-#include "ring_stage.cuh"
+#include "../../include/b200ring_device.cuh"
 
 using namespace b200ring;
 
@@ -77,6 +77,10 @@ struct DevGuard {
 // advances table k-1 by one more zero byte.  Kernels consume 4 bytes per step.
 // Slicing-by-4 tables (kCrcTableWords), then kCrcPowWords powers
 // x^(2^n) mod P (reflected) for combining CRCs of adjacent byte ranges.
+// The GF(2) multiply and the x^(2^n) table follow zlib's crc32_combine
+// construction (multmodp / x2nmodp, zlib 1.2.12+, (C) 1995-2022 Jean-loup
+// Gailly and Mark Adler, zlib license; an independent rewrite of that
+// canonical routine).
 static uint32_t gf2_mulmod(uint32_t a, uint32_t b) {
   uint32_t m = 1u << 31, p = 0;
   for (;;) {

@@ -6,26 +6,10 @@
 #include <cuda_runtime.h>
 
 #include "../../include/b200ring.h"
-#include "ring_device.cuh"
+#include "../../include/b200ring_layout.cuh"
 
 namespace b200ring {
 
-// Mirror word: head | kMirrorValid once the consumer has bound the mirror.
-constexpr uint64_t kMirrorValid = 1ull << 63;
-
-// Producer-local state of one attachment (one producer -> one ring channel),
-// allocated on the producer GPU and exported to the consumer by CUDA IPC so
-// that the consumer's release can push the head into `mirror_head` (the
-// credit direction of the double ring, R1).
-struct alignas(128) DestState {
-  uint64_t mirror_head;  // written by the consumer (NVLink store); read locally by the leader
-  uint64_t _p0[15];
-  uint64_t tail_cache;   // SPSC: tail after the last planned entry (leader-owned)
-  uint64_t chan_seq;     // next header seq of this channel (R18)
-  uint64_t lock_acq;     // fault-tolerant rings: lock acquisitions by this attachment
-  uint64_t _p1[13];
-};
-static_assert(sizeof(DestState) == 256, "DestState layout");
 
 // A destination ring as seen by a producer.
 struct DestDesc {

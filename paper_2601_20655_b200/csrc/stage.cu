@@ -6,7 +6,8 @@
 // decoder writing frames).
 #include <cuda_bf16.h>
 
-#include "ring_stage.cuh"
+#include "ring_internal.h"
+#include "../../include/b200ring_device.cuh"
 
 namespace b200ring {
 
