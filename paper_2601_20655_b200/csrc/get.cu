@@ -133,6 +133,7 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
     }
     if (in && ismsg) {
       ring_view_t* v = a.views + mi;
+      RING_CHECK(mi < a.n && start % kAlign == 0 && start + f <= a.R && f >= kHdr, "received entry inside R", start, f);
       v->offset = start + kHdr;
       v->len = len;
       v->footprint = f;
@@ -174,6 +175,7 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
         Plan& p = ctx->plan[item % kPlanRing];
         p.src = reinterpret_cast<uint64_t>(a.data + start + kHdr);
         p.dst = reinterpret_cast<uint64_t>(a.dst + (uint64_t)mi * a.dst_stride);
+        RING_CHECK(mi < a.n && (!deliver || len <= a.dst_stride), "copy-out inside dst", mi, len);
         p.len = deliver ? len : 0;
         p.nunits = nu;
         p.first_unit = units + nu_incl - nu;

@@ -787,6 +787,9 @@ __device__ __forceinline__ void leader_batch(const PutArgs& a, const BatchRef& B
         const uint64_t f = brief[lane].f;
         p.src = mp->src;
         p.dst = reinterpret_cast<uint64_t>(D.data + o.start + kHdr);
+        RING_CHECK(o.start % kAlign == 0 && o.start + f <= D.R && kHdr + len <= f, "put entry inside R", o.start, f);
+        RING_CHECK(o.item - ld_acquire_gpu32(&S->pub_seq) < (uint32_t)kPlanRing, "plan slot free", o.item,
+                   ld_acquire_gpu32(&S->pub_seq));
         p.len = len;
         p.start = o.start;
         p.slot = o.slot;
@@ -937,6 +940,7 @@ __device__ __forceinline__ void write_header(const PutArgs& a, LaunchCtx* ctx, u
     w[14] = (uint32_t)t;
     w[15] = (uint32_t)(t >> 32);
     uint8_t* hd = D.data + ld_cg64(&p.start);
+    RING_CHECK(ld_cg64(&p.start) + kHdr <= D.R, "header inside R", ld_cg64(&p.start), D.R);
 #pragma unroll
     for (int q = 0; q < 4; ++q) st16(hd + 16 * q, make_int4((int)w[4 * q], (int)w[4 * q + 1], (int)w[4 * q + 2], (int)w[4 * q + 3]));
   }
@@ -1212,6 +1216,7 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
       SpecItem& it = sp->it[k0 + lane];
       it.src = src;
       it.dst = reinterpret_cast<uint64_t>(D.data + r.start + kHdr);
+      RING_CHECK(r.start + footprint(len) <= D.R, "speculative entry inside R", r.start, len);
       it.len = len;
       it.first_unit = units + r.fu_off;
       it.nunits = r.nu;

@@ -211,6 +211,7 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
     const uint64_t lo = (uint64_t)c * chunk;
     const uint64_t hi = min(len, lo + chunk);
     if (tr && lane == 0) tr[2] = globaltimer();
+    RING_CHECK(c < (uint32_t)((len + chunk - 1) / chunk) || len == 0, "unit inside its item", u, item);
     if (hi > lo) warp_copy<V>(reinterpret_cast<const uint8_t*>(src) + lo, reinterpret_cast<uint8_t*>(dst) + lo, hi - lo, lane);
     __syncwarp();
     if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);

@@ -3,12 +3,32 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "../../include/b200ring.h"
 #include "../../include/b200ring_layout.cuh"
 
 namespace b200ring {
+
+// Device-side invariant checks (compute-sanitizer is not available on this
+// pool): built with B200RING_NVCC_DEFINES=-DB200RING_CHECKS, a violated bound
+// prints the site and traps, which fails the launch (RING_ECUDA / a CUDA
+// error at the next synchronisation).  Compiled out otherwise.
+#ifdef B200RING_CHECKS
+#define RING_CHECK(cond, what, x, y)                                                              \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("B200RING_CHECK failed: %s (%s:%d) %llu %llu\n", what, __FILE__, __LINE__,            \
+             (unsigned long long)(x), (unsigned long long)(y));                                   \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define RING_CHECK(cond, what, x, y) \
+  do {                               \
+  } while (0)
+#endif
 
 
 // A destination ring as seen by a producer.
