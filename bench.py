@@ -140,7 +140,24 @@ def oracle_pass(msgs, R_bytes, N_slots):
     return sim
 
 
-def cpu_baseline(payload_lens, R_bytes, N_slots, budget_s: float):
+def cpu_baseline(R_bytes, N_slots, producers, per, lo, hi, budget_s: float, what: str):
+    """The CPU baseline of BASELINE.md §6: oracle/ring_threaded.cpp (the same
+    protocol over host memory, one pinned thread per producer plus the
+    consumer, memcpy payloads, std::atomic acquire/release) on a bounded sample
+    of the workload; the single-thread Python stepper's rate is kept beside it."""
+    from oracle import threaded as T
+    r = T.run(R_bytes, N_slots, producers, per, lo, hi, 20260120)
+    py = cpu_baseline_python([lo] * 16 if lo == hi else [lo, hi] * 8, R_bytes, N_slots, budget_s)
+    return {"value": round(r["gbs"], 4), "unit": UNIT, "cores": r["threads"], "kind": "oracle-threaded",
+            "sample": f"{r['messages']} messages ({what}) through oracle/ring_threaded.cpp: {producers} producer "
+                      f"thread(s) + 1 consumer thread, pinned, R={R_bytes >> 20} MiB, N={N_slots}, {r['seconds']:.2f} s"
+                      f"{'' if r['bad'] == 0 else ', DELIVERY ERRORS'}",
+            "msgs_per_s": r["msgs_per_s"], "p50_us": r["p50_us"], "p99_us": r["p99_us"],
+            "cpu_model": r["cpu_model"], "host_cpus": os.cpu_count(), "delivery_ok": r["bad"] == 0,
+            "python_oracle": py}
+
+
+def cpu_baseline_python(payload_lens, R_bytes, N_slots, budget_s: float):
     msgs = oracle_inputs(payload_lens)
     t0 = time.perf_counter()
     n = 0
@@ -395,7 +412,7 @@ def bench_c2(args):
     if engine:
         R.ring_peer_engine_stop(peer, sp)
         sync()
-    cpu = cpu_baseline([plen] * 16, Rb, N, args.cpu_budget)
+    cpu = cpu_baseline(Rb, N, 1, 2000, plen, plen, args.cpu_budget, "C2 shape: 1,048,512-B payloads")
     R.ring_detach(peer)
     R.ring_destroy(ring)
     return {
@@ -576,7 +593,8 @@ def bench_pairs(args, rank, world, grp):
     dist.all_gather_object(gathered, (lat_loaded, unl[4096], unl[C3_LENS[0]]), group=grp)
     cpu = None
     if rank == 0:
-        cpu = cpu_baseline(list(C3_LENS) * 4, Rb, N, args.cpu_budget)
+        cpu = cpu_baseline(Rb, N, 1, 500, C3_LENS[1], C3_LENS[0], args.cpu_budget,
+                           "C3 shape: U[4,193,280, 4,194,304]-B payloads")
     dist.barrier(group=grp)
     R.ring_detach(peer)
     dist.barrier(group=grp)
@@ -630,25 +648,29 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
+    from oracle import threaded as T
     if world == 1:
-        lens, Rb, N, wl = [1048512] * 16, 64 << 20, 64, "C2 sample: 16 x 1,048,512-B messages per step"
+        lo = hi = 1048512
+        per, Rb, N, wl = 64, 64 << 20, 64, "C2 sample: 64 x 1,048,512-B messages per step (one ring's worth)"
     else:
-        lens, Rb, N, wl = list(C3_LENS) * 4, 64 << 20, 64, "C3 sample: 8 x ~4 MiB messages per step"
-    msgs = oracle_inputs(lens)
-    times = []
+        lo, hi = C3_LENS[1], C3_LENS[0]
+        per, Rb, N, wl = 16, 64 << 20, 64, "C3 sample: 16 x ~4 MiB messages per step"
+    times, nbytes, res = [], 0, None
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        oracle_pass(msgs, Rb, N)
+        res = T.run(Rb, N, 1, per, lo, hi, 20260120 + i)
         if i >= args.warmup:
-            times.append(time.perf_counter() - t0)
+            times.append(res["seconds"])
+            nbytes += res["bytes"]
     tot = sum(times)
-    value = sum(lens) * len(times) / tot / 1e9
+    value = nbytes / tot / 1e9
     return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / len(times) * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl, "R_bytes": Rb, "n_slots": N},
-            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": wl + " through oracle/ring.py (single thread)"},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": res["threads"],
+                             "kind": "oracle-threaded", "cpu_model": res["cpu_model"], "host_cpus": os.cpu_count(),
+                             "sample": wl + " through oracle/ring_threaded.cpp (1 producer + 1 consumer thread, "
+                                            "pinned, memcpy payloads)"},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
