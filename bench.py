@@ -325,9 +325,28 @@ def bench_c2(args):
     clocks = clk.stop()
     ms = t_start.elapsed_time(t_end)
     args.steps = steps
-    assert (status == 0).all().item()
+    assert (status.cpu() == 0).all()
     v = R.parse_views(views.cpu().numpy())
     assert (v["status"] == 0).all()
+    # repetitions (5 runs, median with min / max): the timed
+    # region above plus 4 more passes of the same K steps, eager launches
+    rep_gbs = [m * plen * steps / (ms / 1e3) / 1e9]
+    for r in range(4):
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sync()
+        r0.record(main)
+        sp.wait_stream(main)
+        sc.wait_stream(main)
+        for i in range(steps):
+            step(i)
+        if engine:
+            R.ring_peer_engine_wait(peer, sp)
+        main.wait_stream(sp)
+        main.wait_stream(sc)
+        r1.record(main)
+        sync()
+        rep_gbs.append(m * plen * steps / (r0.elapsed_time(r1) / 1e3) / 1e9)
+    assert (status.cpu() == 0).all()
     # loaded latency, pooled over >= 1,000 messages: a further
     # streaming pass (outside the timed region) with one view buffer per step,
     # first 10 % dropped as warm-up
@@ -344,6 +363,53 @@ def bench_c2(args):
         lat_all += ((vv["t_visible"].astype(np.int64) - tp) / 1e3).tolist()
     lat_us = lat_all[len(lat_all) // 10:]
     del lviews
+
+    # unloaded latency: one message in flight, put -> consume,
+    # t_visible - t_put (t_put: the put's leader takes the message up, before
+    # the claim); 4 KiB, the C2 payload and a C3-sized 4 MiB payload
+    log("C2: unloaded latency, flag round trip, small messages")
+    unl = {}
+    one_v = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    one_st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for size in (4096, plen, 4194304 - 64):
+        one = R.make_msgs([src.data_ptr()], [size], [bytes(16)], [0], [7], [1])
+        d_one = torch.from_numpy(one.view(np.uint8).copy()).cuda()
+        lat = []
+        for i in range(110):
+            R.ring_consume(ring, 1, one_v, None, 0, 0, sc)     # the consumer waits for it
+            R.ring_put_batch(peer, d_one, 1, 0, one_st, sp)
+            sync()
+            vv = R.parse_views(one_v.cpu().numpy())
+            tp = int(np.frombuffer(vv["header"][0, 56:64].tobytes(), dtype="<u8")[0])
+            lat.append((int(vv["t_visible"][0]) - tp) / 1e3)
+        unl[size] = lat[10:]
+    # flag round trip between two kernels on this GPU: the
+    # small-message roofline msgs/s <= 1 / (t_RTT * k), k = 1 for SPSC
+    rtt = R.ring_probe_rtt(dev, dev, 2000)
+    # small messages streaming: 4 KiB, 1,024 per step (view consume)
+    small_m, small_steps = 1024, 20
+    smalls = R.make_msgs([src.data_ptr() + 4096 * q for q in range(small_m)], [4096] * small_m,
+                         [bytes(16)] * small_m, [0] * small_m, [7] * small_m, [1] * small_m)
+    d_small = torch.from_numpy(smalls.view(np.uint8).copy()).cuda()
+    small_st = torch.zeros(small_m, dtype=torch.int32, device="cuda")
+    small_v = torch.zeros(small_m * 128, dtype=torch.uint8, device="cuda")
+    for i in range(3):
+        R.ring_put_batch(peer, d_small, small_m, 0, small_st, sp)
+        R.ring_consume(ring, small_m, small_v, None, 0, 0, sc)
+    sync()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(main)
+    sp.wait_stream(main)
+    sc.wait_stream(main)
+    for i in range(small_steps):
+        R.ring_put_batch(peer, d_small, small_m, 0, small_st, sp)
+        R.ring_consume(ring, small_m, small_v, None, 0, 0, sc)
+    main.wait_stream(sp)
+    main.wait_stream(sc)
+    s1.record(main)
+    sync()
+    small_ok = bool((small_st.cpu() == 0).all()) and bool((R.parse_views(small_v.cpu().numpy())["status"] == 0).all())
+    small_msgs_s = small_m * small_steps / (s0.elapsed_time(s1) / 1e3)
 
     payload = m * plen * args.steps
     value = payload / (ms / 1e3) / 1e9
@@ -431,6 +497,23 @@ def bench_c2(args):
         "latency_us": {"p50": pct(lat_us, 50), "p99": pct(lat_us, 99), "samples": len(lat_us),
                        "what": "loaded: t_visible - t_put over 20 streamed steps (first 10 % dropped; same GPU "
                                "clock; batched put, so it includes the wait behind earlier messages of the batch)"},
+        "repetitions": {"n": len(rep_gbs), "median": round(statistics.median(rep_gbs), 2),
+                        "min": round(min(rep_gbs), 2), "max": round(max(rep_gbs), 2), "unit": UNIT,
+                        "what": "the timed region plus 4 more passes of the same K steps"},
+        "latency_unloaded_us": {
+            f"{s}B": {"p50": pct(l, 50), "p99": pct(l, 99), "samples": len(l)} for s, l in unl.items()} | {
+            "what": "one message in flight (the consumer already waiting), t_visible - t_put, t_put = the "
+                    "put leader taking the message up (before the claim); first 10 of 110 dropped"},
+        "small_messages": {"size": 4096, "msgs_per_s": round(small_msgs_s, 1), "ok": small_ok,
+                           "rtt_min_us": round(rtt["rtt_min_ns"] / 1e3, 3),
+                           "rtt_p50_us": round(rtt["rtt_p50_ns"] / 1e3, 3),
+                           "unbatched_bound_msgs_per_s": round(1e9 / rtt["rtt_p50_ns"], 1),
+                           "ratio_to_unbatched_bound": round(small_msgs_s / (1e9 / rtt["rtt_p50_ns"]), 3),
+                           "what": "4 KiB messages, 1,024 per put launch, streamed 20 launches.  SURVEY.md d-3's "
+                                   "bound 1 / (t_RTT * k), k = 1 (SPSC), holds for one message per publication; "
+                                   "the put publishes a run of complete entries with one fence, so a batch "
+                                   "exceeds it by the run length.  t_RTT = median in-run flag round trip between "
+                                   "two kernels on this GPU (ring_probe_rtt, system scope)"},
         "kernels_ms": {"put_avg": round(put_avg_ms, 5), "consume_avg": round(statistics.mean(get_ms), 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("ncu_put_c2.json"),

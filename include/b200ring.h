@@ -419,6 +419,16 @@ uint64_t ring_launch_count(void);
  * between two GPUs of one host be computed on one time base.  Synchronous,
  * ~3 ms. */
 ring_status_t ring_clock_offset_ns(int device, int64_t* offset_ns);
+/* Measurement support: `iters` flag round trips
+ * between one thread on `dev_a` and one on `dev_b` (dev_a == dev_b: two kernels
+ * on one GPU), each polling a word in its own memory that the other stores to
+ * with system-scope release / acquire -- the ring's signalling pattern.  First
+ * 10 % dropped.  Returns the minimum and median round trip, and (if not NULL)
+ * the NTP-style offset of dev_b's %globaltimer minus dev_a's from the
+ * minimum-RTT round (pong's stamp - (ping's send + RTT/2)), a cross-check of
+ * ring_clock_offset_ns.  Synchronous.  RING_ETIMEDOUT if a side stalled (2 s). */
+ring_status_t ring_probe_rtt(int dev_a, int dev_b, uint32_t iters, uint64_t* rtt_min_ns, uint64_t* rtt_p50_ns,
+                            int64_t* offset_b_minus_a_ns);
 /* Footprint of a payload: align_up(64 + len, 128) (R9, R11). */
 uint64_t ring_footprint(uint64_t len);
 

@@ -298,6 +298,75 @@ ring_status_t ring_clock_offset_ns(int device, int64_t* offset_ns) {
   g_launches++;
   return RING_OK;
 }
+ring_status_t ring_probe_rtt(int dev_a, int dev_b, uint32_t iters, uint64_t* rtt_min_ns, uint64_t* rtt_p50_ns,
+                            int64_t* offset_b_minus_a_ns) {
+  if (!rtt_min_ns || !rtt_p50_ns || iters == 0 || iters > (1u << 20)) return RING_EINVAL;
+  const uint32_t* unused = nullptr;
+  ring_status_t s = crc_table_dev(dev_a, &unused);   // loads the kernels
+  if (s == RING_OK) s = crc_table_dev(dev_b, &unused);
+  if (s != RING_OK) return s;
+  s = enable_peer(dev_a, dev_b);
+  if (s == RING_OK) s = enable_peer(dev_b, dev_a);
+  if (s != RING_OK) return s;
+  uint64_t *fa = nullptr, *fb = nullptr, *ta = nullptr, *rt = nullptr, *tb = nullptr;
+  cudaStream_t sa = nullptr, sb = nullptr;
+  {
+    DevGuard g(dev_a);
+    CUDA_TRY(cudaMalloc(&fa, 256));
+    CUDA_TRY(cudaMemset(fa, 0, 256));
+    CUDA_TRY(cudaMalloc(&ta, 16ull * iters));
+    rt = ta + iters;
+    CUDA_TRY(cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking));
+  }
+  {
+    DevGuard g(dev_b);
+    CUDA_TRY(cudaMalloc(&fb, 256));
+    CUDA_TRY(cudaMemset(fb, 0, 256));
+    CUDA_TRY(cudaMalloc(&tb, 8ull * iters));
+    CUDA_TRY(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
+    CUDA_TRY(quiesce());                                                   // the flags are zero
+  }
+  {
+    DevGuard g(dev_a);
+    CUDA_TRY(quiesce());
+    CUDA_TRY(cudaMemset(ta, 0, 16ull * iters));
+    CUDA_TRY(quiesce());
+  }
+  {
+    DevGuard g(dev_b);
+    CUDA_TRY(launch_probe_pong(fa, fb, iters, tb, 2000000000ull, sb));   // pong first: it waits
+  }
+  {
+    DevGuard g(dev_a);
+    CUDA_TRY(launch_probe_ping(fb, fa, iters, ta, rt, 2000000000ull, sa));
+    CUDA_TRY(cudaStreamSynchronize(sa));
+  }
+  {
+    DevGuard g(dev_b);
+    CUDA_TRY(cudaStreamSynchronize(sb));
+  }
+  std::vector<uint64_t> hs(iters), hr(iters), hb(iters);
+  CUDA_TRY(cudaMemcpy(hs.data(), ta, 8ull * iters, cudaMemcpyDefault));
+  CUDA_TRY(cudaMemcpy(hr.data(), rt, 8ull * iters, cudaMemcpyDefault));
+  CUDA_TRY(cudaMemcpy(hb.data(), tb, 8ull * iters, cudaMemcpyDefault));
+  { DevGuard g(dev_a); cudaFree(fa); cudaFree(ta); cudaStreamDestroy(sa); }
+  { DevGuard g(dev_b); cudaFree(fb); cudaFree(tb); cudaStreamDestroy(sb); }
+  g_launches += 2;
+  // the first 10 % are warm-up; NTP-style offset from the minimum-RTT round
+  const uint32_t w = iters / 10;
+  std::vector<uint64_t> r(hr.begin() + w, hr.end());
+  if (r.empty() || *std::min_element(r.begin(), r.end()) == 0) return RING_ETIMEDOUT;
+  uint32_t best = w;
+  for (uint32_t i = w; i < iters; ++i)
+    if (hr[i] < hr[best]) best = i;
+  std::sort(r.begin(), r.end());
+  *rtt_min_ns = r.front();
+  *rtt_p50_ns = r[r.size() / 2];
+  if (offset_b_minus_a_ns)
+    *offset_b_minus_a_ns = (int64_t)hb[best] - (int64_t)(hs[best] + hr[best] / 2);
+  return RING_OK;
+}
+
 uint64_t ring_footprint(uint64_t len) { return footprint(len); }
 
 // ---- lifetime ------------------------------------------------------------------

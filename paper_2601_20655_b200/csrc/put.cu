@@ -722,6 +722,8 @@ __device__ __forceinline__ void leader_batch(const PutArgs& a, const BatchRef& B
       brief[lane].nunits = units_for(len, a.chunk);
       brief[lane].t_arr = mp->hdr.accepted_at;
     }
+    // t_put of the round's messages: the leader takes them up now, before any claim
+    const uint64_t t_in = __shfl_sync(0xffffffffu, (B.flags & RING_NO_TIMESTAMP) ? 0ull : globaltimer(), 0);
     uint64_t tc = 0, cq = 0;   // issued together with the brief loads (first round)
     if (lane == 0 && fast && !(L.loaded & 1u)) {
       tc = a.dest0.st->tail_cache;
@@ -780,6 +782,7 @@ __device__ __forceinline__ void leader_batch(const PutArgs& a, const BatchRef& B
       p.nunits = o.nunits;
       p.first_unit = o.first_unit;
       p.len = 0;
+      p.t_in = t_in;
       if (o.status == RING_OK) {
         const ring_msg_t* mp = B.msgs ? B.msgs + k : &a.inline_msg;
         const DestDesc& D = s_dests[o.dest];
@@ -936,7 +939,7 @@ __device__ __forceinline__ void write_header(const PutArgs& a, LaunchCtx* ctx, u
     w[12] = ld_cg32(&p.seq);
     w[13] = ld_cg32(&p.epoch) & 0xffffu;   // epoch[52,54) flags[54,56)
     w[0] = crc52(w, crc_tab);
-    const uint64_t t = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();
+    const uint64_t t = ld_cg64(&p.t_in);    // t_put: when the leader took the message up (0: RING_NO_TIMESTAMP)
     w[14] = (uint32_t)t;
     w[15] = (uint32_t)(t >> 32);
     uint8_t* hd = D.data + ld_cg64(&p.start);

@@ -79,7 +79,8 @@ struct alignas(64) Plan {
   uint64_t start;                   // put: entry offset in the data region (header goes to data + start)
   uint64_t msgp;                    // put engine: the message descriptor (header fields) of this item
   uint64_t statusp;                 // put engine: its status word
-  uint64_t _p[2];
+  uint64_t t_in;                    // put: %globaltimer when the leader took the message up (header t_put)
+  uint64_t _p[1];
   uint32_t _h[16];
 };
 static_assert(sizeof(Plan) == 192, "Plan layout");
@@ -276,6 +277,10 @@ cudaError_t launch_release(const ReleaseArgs& a, cudaStream_t s);
 cudaError_t launch_engine_doorbell(EngineQueue* q, uint64_t b, const ring_msg_t* msgs, uint32_t* status, uint32_t n,
                                    uint32_t flags, bool wait, uint64_t timeout_ns, cudaStream_t s);
 cudaError_t launch_engine_stop(EngineQueue* q, cudaStream_t s);
+cudaError_t launch_probe_ping(uint64_t* remote, const uint64_t* local, uint32_t iters, uint64_t* t_send,
+                              uint64_t* rtt, uint64_t timeout_ns, cudaStream_t s);
+cudaError_t launch_probe_pong(uint64_t* remote, const uint64_t* local, uint32_t iters, uint64_t* t_seen,
+                              uint64_t timeout_ns, cudaStream_t s);
 cudaError_t launch_engine_wait(EngineQueue* q, uint64_t upto, uint64_t timeout_ns, cudaStream_t s);
 // Load a kernel on the current device now and give it the ring's shared-memory
 // carveout.  Lazy loading: a module loaded at first launch waits for the

@@ -104,6 +104,7 @@ def _load():
         "ring_put_routed": [P, P, U32, U32, P, P, P],
         "ring_set_timeout_ns": [U64],
         "ring_clock_offset_ns": [I, C.POINTER(C.c_int64)],
+        "ring_probe_rtt": [I, I, U32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int64)],
         "ring_peer_trace": [P, P, U32],
         "ring_peer_set_fault": [P, C.POINTER(ring_fault_t)],
         "ring_set_lock_timeout_ns": [U64],
@@ -311,6 +312,12 @@ def ring_put_routed(router: int, d_msgs, n: int, flags: int, d_status, d_dest=No
 # ---- misc ---------------------------------------------------------------------------------
 def ring_set_timeout_ns(ns: int) -> None:
     _check("ring_set_timeout_ns", lib.ring_set_timeout_ns(ns))
+
+
+def ring_probe_rtt(dev_a: int, dev_b: int, iters: int = 1000) -> dict:
+    mn, p50, off = C.c_uint64(), C.c_uint64(), C.c_int64()
+    _check("ring_probe_rtt", lib.ring_probe_rtt(dev_a, dev_b, iters, C.byref(mn), C.byref(p50), C.byref(off)))
+    return {"rtt_min_ns": mn.value, "rtt_p50_ns": p50.value, "offset_b_minus_a_ns": off.value}
 
 
 def ring_clock_offset_ns(device: int) -> int:
