@@ -675,7 +675,11 @@ def bench_pairs(args, rank, world, grp):
     gathered = [None] * world
     dist.all_gather_object(gathered, (lat_loaded, unl[4096], unl[C3_LENS[0]]), group=grp)
     cpu = None
+    ce, rtt = None, None
     if rank == 0:
+        ce = measure_ce(dev, (dev + 1) % torch.cuda.device_count())
+        rtt = R.ring_probe_rtt(dev, (dev + 1) % torch.cuda.device_count(), 2000)
+        rtt["host_mapped_offset_ns"] = int(offsets[1] - offsets[0])
         cpu = cpu_baseline(Rb, N, 1, 500, C3_LENS[1], C3_LENS[0], args.cpu_budget,
                            "C3 shape: U[4,193,280, 4,194,304]-B payloads")
     dist.barrier(group=grp)
@@ -702,6 +706,14 @@ def bench_pairs(args, rank, world, grp):
                    "parallelism": f"{world} concurrent SPSC rings (one egress + one ingress stream per GPU)"},
         "per_gpu_gbs": round(per_gpu, 2),
         "nvlink_frac_of_900": round(per_gpu / NVLINK_NOMINAL, 4),
+        "nvlink_ce": ce,
+        "nvlink_frac_of_ce": round(per_gpu / ce["bidir_per_direction_gbs"], 4) if ce else None,
+        "flag_rtt": {"rtt_min_us": round(rtt["rtt_min_ns"] / 1e3, 3), "rtt_p50_us": round(rtt["rtt_p50_ns"] / 1e3, 3),
+                     "ntp_offset_ns": rtt["offset_b_minus_a_ns"], "host_mapped_offset_ns": rtt["host_mapped_offset_ns"],
+                     "offset_disagreement_ns": rtt["offset_b_minus_a_ns"] - rtt["host_mapped_offset_ns"],
+                     "what": "flag ping-pong GPU r <-> GPU r+1 (ring_probe_rtt, system scope, 2,000 rounds): RTT, "
+                             "and the NTP-style clock offset from the min-RTT round next to the host-mapped offset "
+                             "(ring_clock_offset_ns) the latencies use"} if rtt else None,
         "msgs_per_s": round(m * args.steps * world / (ms_max / 1e3), 1),
         "latency_us": {
             "loaded_p50": pct(loaded, 50), "loaded_p99": pct(loaded, 99),
@@ -711,10 +723,13 @@ def bench_pairs(args, rank, world, grp):
             "what": "t_visible (consumer GPU) - t_put (producer GPU), both %globaltimer mapped to the host "
                     "CLOCK_MONOTONIC with ring_clock_offset_ns; loaded = 20 streamed steps after the timed "
                     "region, unloaded = one message in flight; first 10 % of each dropped"},
-        "roofline": {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": NVLINK_PEAK_MEASURED, "unit": "GB/s",
-                     "frac": round(per_gpu / NVLINK_PEAK_MEASURED, 4), "traffic": None, "kernel": "put_kernel",
-                     "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction (900 nominal); "
-                                    "SM peer-store ceiling measured here 690-695 GB/s"},
+        "roofline": {"bound": "nvlink", "achieved": round(per_gpu, 1),
+                     "peak": ce["bidir_per_direction_gbs"] if ce else NVLINK_PEAK_MEASURED, "unit": "GB/s",
+                     "frac": round(per_gpu / (ce["bidir_per_direction_gbs"] if ce else NVLINK_PEAK_MEASURED), 4),
+                     "traffic": None, "kernel": "put_kernel<2>",
+                     "peak_source": ("in-run cudaMemcpyPeerAsync, both directions at once (nvlink_ce); "
+                                     if ce else "B200_PROFILING.md measured peer copy 770 GB/s; ") +
+                                    "900 GB/s nominal per direction: nvlink_frac_of_900"},
         "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": m * stride * world,
                 "d2h_bytes_per_step": m * 128 * world},
         "gpu_launches": int(summary[3]) * world,
@@ -722,6 +737,53 @@ def bench_pairs(args, rank, world, grp):
         "cpu_baseline": cpu,
         "ok": bad == 0.0,
     }
+
+
+def measure_ce(a: int, b: int, nbytes: int = 256 << 20, reps: int = 10) -> dict:
+    """In-run copy-engine NVLink peak (cudaMemcpyPeerAsync via torch copies):
+    GPU a -> GPU b alone, and a -> b with b -> a at the same time."""
+    import torch
+    x = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{a}")
+    y = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{b}")
+    x2 = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{b}")
+    y2 = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{a}")
+    sa, sb = torch.cuda.Stream(a), torch.cuda.Stream(b)
+    for _ in range(2):
+        with torch.cuda.stream(sa):
+            y.copy_(x, non_blocking=True)
+    torch.cuda.synchronize(a)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(sa):
+        e0.record(sa)
+        for _ in range(reps):
+            y.copy_(x, non_blocking=True)
+        e1.record(sa)
+    torch.cuda.synchronize(a)
+    one = nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(sa):
+        f0.record(sa)
+        for _ in range(reps):
+            y.copy_(x, non_blocking=True)
+        f1.record(sa)
+    with torch.cuda.device(b), torch.cuda.stream(sb):
+        g0.record(sb)
+        for _ in range(reps):
+            y2.copy_(x2, non_blocking=True)
+        g1.record(sb)
+    torch.cuda.synchronize(a)
+    torch.cuda.synchronize(b)
+    bi = min(nbytes * reps / (f0.elapsed_time(f1) / 1e3) / 1e9, nbytes * reps / (g0.elapsed_time(g1) / 1e3) / 1e9)
+    del x, y, x2, y2
+    return {"one_direction_gbs": round(one, 1), "bidir_per_direction_gbs": round(bi, 1),
+            "what": f"cudaMemcpyPeerAsync {nbytes >> 20} MiB x {reps}, GPU {a} -> {b} alone and with {b} -> {a} "
+                    "concurrently (min of the two directions)"}
+
+
+def R_clock_offset(dev):
+    from paper_2601_20655_b200 import ring as R
+    return R.ring_clock_offset_ns(dev)
 
 
 def reference_arm(args):
@@ -808,6 +870,10 @@ def main():
     # NCCL is the process group of record; the handle exchange and the
     # max-over-ranks reduction run on a gloo group (CPU objects only).
     dist.init_process_group("nccl")
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    import torch
+    torch.cuda.set_device(local)
+    dist.barrier(device_ids=[local])      # once, off the data path: NCCL saw every rank
     grp = dist.new_group(backend="gloo")
     try:
         if args.topology != "pairs":
@@ -817,6 +883,29 @@ def main():
             out = bench_multi.main(args, rank, world, grp)
         else:
             out = bench_pairs(args, rank, world, grp)
+            # the configs BASELINE.json maps to this GPU count, in the
+            # same line: C4 at >= 4 GPUs, C5a (verified sweep) and C5b (verified flip)
+            # at >= 3 (the 8-GPU shape is 7 producers -> 1 consumer)
+            import copy
+            import bench_multi
+            extra = {}
+            offsets = [None] * world
+            dist.all_gather_object(offsets, R_clock_offset(local), group=grp)
+            if world >= 4:
+                a4 = copy.copy(args)
+                a4.steps, a4.warmup, a4.msgs_per_step = 10, 3, 2
+                extra["c4"] = bench_multi.run_pipeline(a4, rank, world, grp, offsets)
+            if world >= 3:
+                a5 = copy.copy(args)
+                a5.sizes, a5.verify, a5.fanin_mode = "4096,4194304,268435456", True, "mpsc"
+                extra["c5a"] = bench_multi.run_fanin(a5, rank, world, grp, offsets)
+                a5b = copy.copy(args)
+                a5b.msgs_per_step, a5b.verify = 48, True
+                extra["c5b"] = bench_multi.run_reassign(a5b, rank, world, grp, offsets)
+            if out is not None:
+                for k, v in extra.items():
+                    if v is not None:
+                        out[k] = v
         if out:
             print(json.dumps(out), flush=True)
     finally:

@@ -74,6 +74,41 @@ def _fill(nbytes, seed):
     return t.view(torch.uint8)[:nbytes]
 
 
+def _seeded_source(nbytes, seed):
+    """A source buffer holding synth.payload_bytes(seed, 0, 0, nbytes) (device
+    generator): every message put from it can be checked on the device."""
+    from synth import device as SD
+    t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    SD.fill([t.data_ptr()], [nbytes], [0], [0], seed)
+    torch.cuda.synchronize()
+    return t
+
+
+def _verify_pass(ring, total, seed, stream):
+    """Consumer side of a verification pass: every entry is taken with ring_get,
+    its payload compared in place (before release) with the generator on the
+    device (synth/csrc/synth_dev.cu), then released.  Returns (bad payloads,
+    per-producer order ok, views)."""
+    from synth import device as SD
+    vt = torch.zeros(total * 128, dtype=torch.uint8, device="cuda")
+    zc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    zs = torch.zeros(1, dtype=torch.int64, device="cuda")
+    base = R.ring_get_info(ring).data
+    bads = []
+    for j in range(total):
+        v = vt[j * 128:(j + 1) * 128]
+        R.ring_get(ring, 1, v, None, 0, 0, stream)
+        bads.append(SD.verify_views(v, 1, base, seed, zc, zs, None, 0, stream))
+        R.ring_release(ring, 1, stream)
+    stream.synchronize()
+    nbad = sum(int((b.cpu() != -1).sum()) for b in bads)
+    vv = _views(vt)
+    pid = np.frombuffer(vv["header"][:, 44:48].tobytes(), dtype="<u4")
+    seq = np.frombuffer(vv["header"][:, 48:52].tobytes(), dtype="<u4")
+    order_ok = all(bool(np.all(np.diff(seq[pid == p].astype(np.int64)) == 1)) for p in np.unique(pid))
+    return nbad, order_ok and bool((vv["status"] == 0).all()), vv
+
+
 def _wire(plan, rank, world, grp, dev):
     return T.wire(plan, rank, world, grp, device=dev,
                   create=lambda s, d: R.ring_create(d, s.data_bytes, s.n_slots, s.max_producers, s.flags),
@@ -167,7 +202,12 @@ def run_fanin(args, rank, world, grp, offsets):
     sizes = [4096 << (2 * i) for i in range(9)]          # 4 KiB .. 256 MiB
     if args.sizes:
         sizes = [int(x) for x in args.sizes.split(",")]
-    src = _fill(256 << 20, 2000 + rank) if rank > 0 else None
+    verify = getattr(args, "verify", False)
+    vseed = synth.SEED_BASE + 5
+    if rank > 0:
+        src = _seeded_source(max(sizes), vseed) if verify else _fill(max(sizes), 2000 + rank)
+    else:
+        src = None
     rows = []
     for size in sizes:
         M = int(min(1000, max(4, (2 << 30) // size // max(1, world - 1))))
@@ -208,11 +248,28 @@ def run_fanin(args, rank, world, grp, offsets):
         ms = float(t[0])
         allb = size * M * (world - 1)
         lat0 = lats[0]
-        rows.append({"size": size, "msgs_per_producer": M, "ms": round(ms, 4),
-                     "ingress_gbs": round(allb / (ms / 1e3) / 1e9, 2),
-                     "msgs_per_s": round(M * (world - 1) / (ms / 1e3), 1),
-                     "lat_p50_us": _pct(lat0, 50), "lat_p99_us": _pct(lat0, 99), "lat_samples": len(lat0),
-                     "ok": float(t[1]) == 0.0})
+        row = {"size": size, "msgs_per_producer": M, "ms": round(ms, 4),
+               "ingress_gbs": round(allb / (ms / 1e3) / 1e9, 2),
+               "msgs_per_s": round(M * (world - 1) / (ms / 1e3), 1),
+               "lat_p50_us": _pct(lat0, 50), "lat_p99_us": _pct(lat0, 99), "lat_samples": len(lat0),
+               "ok": float(t[1]) == 0.0}
+        if verify and not lockfree:
+            # verification pass (untimed): the same puts again; every payload
+            # compared in place on the device, per-producer order from the headers
+            dist.barrier(group=grp)
+            vres = [0, 1]
+            if rank == 0:
+                nbad, order_ok, _ = _verify_pass(wired.rings["fan0"], M * (world - 1), vseed, s)
+                vres = [nbad, 1 if order_ok else 0]
+            else:
+                R.ring_put_batch(wired.peers[my_ring], d_msgs, M, 0, st, s)
+                s.synchronize()
+                vres = [0, 1 if bool((st == 0).all().item()) else 0]
+            vt_ = torch.tensor([vres[0], 1 - vres[1]], dtype=torch.float64)
+            dist.all_reduce(vt_, op=dist.ReduceOp.MAX, group=grp)
+            row["verified"] = {"payload_mismatches": int(vt_[0]), "order_and_status_ok": float(vt_[1]) == 0.0,
+                               "what": "second pass, ring_get -> device compare in place -> ring_release per entry"}
+        rows.append(row)
     if rset is not None:
         R.ring_set_destroy(rset)
     _teardown(wired, grp)
@@ -246,7 +303,10 @@ def run_reassign(args, rank, world, grp, offsets):
     M = args.msgs_per_step or 200                           # per producer, even
     half = M // 2
     lens = [EMB, synth.wan_bytes("latent_480p")]
-    src = _fill(EMB, 3000 + rank) if rank > 0 else None
+    verify = getattr(args, "verify", False)
+    vseed = synth.SEED_BASE + 6
+    src = (_seeded_source(EMB, vseed) if verify else _fill(EMB, 3000 + rank)) if rank > 0 else None
+    vres = {}
     router = None
     if 0 < rank:
         router = R.router_create(dev, 4)
@@ -266,14 +326,24 @@ def run_reassign(args, rank, world, grp, offsets):
     e0.record(s)
     if rank == 0:
         vt = torch.zeros(fan0_total * 128, dtype=torch.uint8, device="cuda")
-        R.ring_consume(wired.rings["fan0"], fan0_total, vt, None, 0, 0, s)
+        if verify:        # every payload compared in place before its release (timed with it)
+            nbad, order_ok, _vv = _verify_pass(wired.rings["fan0"], fan0_total, vseed, s)
+            vt = torch.from_numpy(np.ascontiguousarray(_vv).view(np.uint8).reshape(-1).copy())
+            vres = {"payload_mismatches": nbad, "order_and_status_ok": order_ok}
+        else:
+            R.ring_consume(wired.rings["fan0"], fan0_total, vt, None, 0, 0, s)
     else:
         R.ring_put_routed(router, d1, half, 0, st[:half], dests[:half], s)
     if rank == spare:
         vt = torch.zeros(fan1_total * 128, dtype=torch.uint8, device="cuda")
         s2 = torch.cuda.Stream()
         s.synchronize()                 # the spare finishes its first half, then becomes a consumer
-        R.ring_consume(wired.rings["fan1"], fan1_total, vt, None, 0, 0, s2)
+        if verify:
+            nbad, order_ok, _vv = _verify_pass(wired.rings["fan1"], fan1_total, vseed, s2)
+            vt = torch.from_numpy(np.ascontiguousarray(_vv).view(np.uint8).reshape(-1).copy())
+            vres = {"payload_mismatches": nbad, "order_and_status_ok": order_ok}
+        else:
+            R.ring_consume(wired.rings["fan1"], fan1_total, vt, None, 0, 0, s2)
         s.wait_stream(s2)
     elif rank > 0:
         # NodeManager reassignment: the new route takes effect for later puts (epoch flip)
@@ -289,7 +359,7 @@ def run_reassign(args, rank, world, grp, offsets):
         ok = bool((v["status"] == 0).all())
         hd = [R.parse_views(vt.cpu().numpy())["header"][i] for i in range(len(v))]
         epochs = [int.from_bytes(bytes(h[52:54]), "little") for h in hd]
-        info = {"received": len(v), "epochs": sorted(set(epochs))}
+        info = {"received": len(v), "epochs": sorted(set(epochs))} | ({"verified": vres} if vres else {})
     if rank > 0:
         ok = ok and bool((st == 0).all().item())
     t = torch.tensor([ms, 0.0 if ok else 1.0], dtype=torch.float64)

@@ -320,13 +320,13 @@ def test_c5b_epoch_flip(R, cross):
     where it stands.  Checked: every message's destination and header epoch as
     predicted from its producer's flip point, per-channel order on both rings,
     the oracle's replay of each ring's observed merge, every payload byte."""
-    devs = devices(5, cross)          # ring A on devs[0], ring B on devs[4], producers devs[1..3]
+    devs = devices(4, cross)          # ring A on devs[0], ring B on devs[3] (P2's GPU, PAPER.md:930-933 shape), producers devs[1..3]
     L = Layout(1 << 30, 256)
     seed, M = synth.SEED_BASE + 6, 24
     half = M // 2
     lens = [(EMB, LAT480)[k % 2] for k in range(M)]
     ringA = R.ring_create(devs[0], L.R, L.N, 3, 0)
-    ringB = R.ring_create(devs[4], L.R, L.N, 2, 0)
+    ringB = R.ring_create(devs[3], L.R, L.N, 2, 0)
     hA, hB = R.ring_export(ringA), R.ring_export(ringB)
     prod = []
     try:
@@ -351,7 +351,7 @@ def test_c5b_epoch_flip(R, cross):
         # predicted (producer, channel seq on that ring) -> the producer's message index k
         ks = {(ridx, p): [k for k, d in enumerate(exp_dest[p]) if d == ridx] for ridx in (0, 1) for p in range(3)}
         luts = []
-        for ridx, dev in ((0, devs[0]), (1, devs[4])):
+        for ridx, dev in ((0, devs[0]), (1, devs[3])):
             t = [0] * (3 * M)
             for p in range(3):
                 for j, k in enumerate(ks[(ridx, p)]):
@@ -360,8 +360,8 @@ def test_c5b_epoch_flip(R, cross):
         nA = sum(len(ks[(0, p)]) for p in range(3))
         nB = sum(len(ks[(1, p)]) for p in range(3))
         vA = torch.zeros(nA * 128, dtype=torch.uint8, device=f"cuda:{devs[0]}")
-        vB = torch.zeros(nB * 128, dtype=torch.uint8, device=f"cuda:{devs[4]}")
-        sA, sB = torch.cuda.Stream(devs[0]), torch.cuda.Stream(devs[4])
+        vB = torch.zeros(nB * 128, dtype=torch.uint8, device=f"cuda:{devs[3]}")
+        sA, sB = torch.cuda.Stream(devs[0]), torch.cuda.Stream(devs[3])
         bads = []
         # consumers first (they wait for data): get -> verify in place -> release, one entry at a time
         for ring, vt, n, s, lut in ((ringA, vA, nA, sA, luts[0]), (ringB, vB, nB, sB, luts[1])):
