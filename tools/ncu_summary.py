@@ -15,7 +15,9 @@ RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
        "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
        "launch__shared_mem_per_block_dynamic", "launch__shared_mem_per_block_static",
-       "smsp__average_warp_latency_issue_stalled_long_scoreboard", "nvltx__bytes.sum", "nvlrx__bytes.sum"]
+       "smsp__average_warp_latency_issue_stalled_long_scoreboard", "nvltx__bytes.sum", "nvlrx__bytes.sum",
+       "nvltx__bytes_data_user.sum", "nvlrx__bytes_data_user.sum", "l1tex__t_bytes.sum",
+       "smsp__pcsamp_warps_issue_stalled_membar", "smsp__average_warps_issue_stalled_membar_per_issue_active.ratio"]
 
 
 def to_bytes(v, unit):
