@@ -545,11 +545,28 @@ def bench_pairs(args, rank, world, grp):
     torch.cuda.set_device(dev)
     Rb, N = 64 << 20, 64
     m = args.msgs_per_step or 32
-    wired = T.wire(T.plan_pairs(world, Rb, N), rank, world, grp, device=dev,
-                   create=lambda s, d: R.ring_create(d, s.data_bytes, s.n_slots, s.max_producers, 0),
-                   export=R.ring_export, attach=R.ring_attach_peer, bind=R.ring_bind_mirror)
-    ring = wired.rings[f"in{rank}"]
-    peer = wired.peers[f"in{(rank + 1) % world}"]
+    pull = bool(args.pull)
+    own = None
+    if pull:
+        # pull placement: each rank's egress ring lives in its OWN memory; the
+        # next rank opens it and pulls every payload over NVLink (ring_open)
+        own = R.ring_create(dev, Rb, N, 1, 0)
+        h = R.ring_export(own)
+        peer, mh = R.ring_attach_peer(h, dev, 0)
+        hs = [None] * world
+        dist.all_gather_object(hs, (h, mh), group=grp)
+        prev = (rank - 1) % world
+        ring = R.ring_open(hs[prev][0], dev)
+        R.ring_bind_mirror(ring, 0, hs[prev][1])
+        if args.cons_ctas or args.cons_threads:
+            R.ring_config(ring, args.cons_ctas, args.cons_threads)
+        dist.barrier(group=grp)
+    else:
+        wired = T.wire(T.plan_pairs(world, Rb, N), rank, world, grp, device=dev,
+                       create=lambda s, d: R.ring_create(d, s.data_bytes, s.n_slots, s.max_producers, 0),
+                       export=R.ring_export, attach=R.ring_attach_peer, bind=R.ring_bind_mirror)
+        ring = wired.rings[f"in{rank}"]
+        peer = wired.peers[f"in{(rank + 1) % world}"]
     if args.ctas or args.threads or args.copy_mode:
         R.ring_peer_config(peer, args.ctas, args.threads, args.copy_mode)
     offsets = [None] * world
@@ -574,10 +591,13 @@ def bench_pairs(args, rank, world, grp):
     payload_step = sum(C3_LENS[q % 2] for q in range(m))
     status = torch.zeros(m, dtype=torch.int32, device="cuda")
     views = torch.zeros(m * 128, dtype=torch.uint8, device="cuda")
+    pull_dst = torch.empty(m * stride, dtype=torch.uint8, device="cuda") if pull else None
     sp, sc = torch.cuda.Stream(), torch.cuda.Stream()
 
     def step(i):
-        R.ring_consume(ring, m, views, None, 0, 0, sc)     # consumer first: it waits for data
+        # consumer first: it waits for data.  Pull: its copy-out brings every
+        # payload over NVLink into pull_dst (push: the put already wrote it here)
+        R.ring_consume(ring, m, views, pull_dst, stride if pull else 0, 0, sc)
         R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
 
     def latencies():
@@ -621,7 +641,7 @@ def bench_pairs(args, rank, world, grp):
     lviews = [torch.zeros(m * 128, dtype=torch.uint8, device="cuda") for _ in range(lat_steps)]
     dist.barrier(group=grp)
     for i in range(lat_steps):
-        R.ring_consume(ring, m, lviews[i], None, 0, 0, sc)
+        R.ring_consume(ring, m, lviews[i], pull_dst, stride if pull else 0, 0, sc)
         R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)
     torch.cuda.synchronize()
     lat_loaded = []
@@ -640,7 +660,7 @@ def bench_pairs(args, rank, world, grp):
         one = torch.from_numpy(R.make_msgs([src.data_ptr()], [size], [bytes(16)], [0], [7], [2]).view(np.uint8).copy()).cuda()
         for it in range(args.lat_iters):
             dist.barrier(group=grp)
-            R.ring_consume(ring, 1, views, None, 0, 0, sc)
+            R.ring_consume(ring, 1, views, pull_dst, stride if pull else 0, 0, sc)
             time.sleep(0.0002)
             R.ring_put_batch(peer, one, 1, 0, status, sp)
             torch.cuda.synchronize()
@@ -661,7 +681,7 @@ def bench_pairs(args, rank, world, grp):
     for i in range(e_steps):
         with torch.cuda.stream(sp):
             src[: m * stride].copy_(host_src, non_blocking=True)
-        R.ring_consume(ring, m, views, None, 0, 0, sc)
+        R.ring_consume(ring, m, views, pull_dst, stride if pull else 0, 0, sc)
         R.ring_put_batch(peer, d_msgs[0], m, 0, status, sp)
         sp.wait_stream(sc)
         with torch.cuda.stream(sp):
@@ -683,9 +703,15 @@ def bench_pairs(args, rank, world, grp):
         cpu = cpu_baseline(Rb, N, 1, 500, C3_LENS[1], C3_LENS[0], args.cpu_budget,
                            "C3 shape: U[4,193,280, 4,194,304]-B payloads")
     dist.barrier(group=grp)
-    R.ring_detach(peer)
-    dist.barrier(group=grp)
-    R.ring_destroy(ring)
+    if pull:
+        R.ring_destroy(ring)            # the mapping of the previous rank's ring
+        dist.barrier(group=grp)
+        R.ring_detach(peer)
+        R.ring_destroy(own)
+    else:
+        R.ring_detach(peer)
+        dist.barrier(group=grp)
+        R.ring_destroy(ring)
     if rank != 0:
         return None
     ms_max, e2e_max, bad = float(summary[0]), float(summary[1]), float(summary[2])
@@ -699,8 +725,11 @@ def bench_pairs(args, rank, world, grp):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "C3-shaped ring of pairs: rank r -> ring on rank (r+1)%N over NVLink, Wan2.1 "
-                               "umT5 emb 512x4096 bf16 / 480p latent 16x21x60x104 bf16 alternating",
+        "config": {"workload": ("C3-shaped ring of pairs, PULL placement: rank r's egress ring lives on rank r, rank "
+                                "(r+1)%N opens it and pulls every payload over NVLink (copy-out consume)" if pull else
+                                "C3-shaped ring of pairs: rank r -> ring on rank (r+1)%N over NVLink") +
+                               ", Wan2.1 umT5 emb 512x4096 bf16 / 480p latent 16x21x60x104 bf16 alternating",
+                   "placement": "pull (ring_open)" if pull else "push (ring at the consumer)",
                    "R_bytes": Rb, "n_slots": N, "msgs_per_step_per_rank": m,
                    "l2": "inputs larger than L2 per rank (2 x 128 MiB source sets)",
                    "parallelism": f"{world} concurrent SPSC rings (one egress + one ingress stream per GPU)"},
@@ -726,7 +755,7 @@ def bench_pairs(args, rank, world, grp):
         "roofline": {"bound": "nvlink", "achieved": round(per_gpu, 1),
                      "peak": ce["bidir_per_direction_gbs"] if ce else NVLINK_PEAK_MEASURED, "unit": "GB/s",
                      "frac": round(per_gpu / (ce["bidir_per_direction_gbs"] if ce else NVLINK_PEAK_MEASURED), 4),
-                     "traffic": None, "kernel": "put_kernel<2>",
+                     "traffic": None, "kernel": "get_kernel<true> copy-out (pull)" if pull else "put_kernel<2>",
                      "peak_source": ("in-run cudaMemcpyPeerAsync, both directions at once (nvlink_ce); "
                                      if ce else "B200_PROFILING.md measured peer copy 770 GB/s; ") +
                                     "900 GB/s nominal per direction: nvlink_frac_of_900"},
@@ -839,6 +868,10 @@ def main():
     ap.add_argument("--lat-iters", type=int, default=560,
                     help="N>1: unloaded-latency round trips per size per rank (>= 1,000 samples pooled at N=2)")
     ap.add_argument("--no-overlap", action="store_true", help="N=1: put(s+1) waits for consume(s)")
+    ap.add_argument("--cons-ctas", type=int, default=0, help="N>1 pull: consumer copy-out grid (0 = default)")
+    ap.add_argument("--cons-threads", type=int, default=0)
+    ap.add_argument("--pull", type=int, default=0,
+                    help="N>1 pairs: 1 = pull placement (ring at the producer, consumer pulls over NVLink)")
     ap.add_argument("--engine", type=int, default=0,
                     help="N=1: 1 = persistent put engine (doorbells), 0 = one put launch per step")
     ap.add_argument("--graph", action="store_true",

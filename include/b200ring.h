@@ -166,6 +166,20 @@ ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uin
                           uint32_t flags, ring_t* out);
 /* Free the ring.  All peers must be detached first (their mappings are borrowed). */
 ring_status_t ring_destroy(ring_t ring);
+/* ring_open: the consumer side of a ring that lives in ANOTHER GPU's memory
+ * (pull placement).  The ring is created (and destroyed, after every ring_open
+ * of it) on the producer's GPU, its producers attach there as usual; the
+ * consumer on `device` opens its handle (same process: peer access; other
+ * process: CUDA IPC) and gets / consumes / releases through the returned
+ * ring_t, whose kernels run on `device` and read the ring over NVLink -- with
+ * copy-out, the payload is pulled into `d_dst` on `device`.  Same protocol and
+ * placements as a ring at the consumer (the oracle does not see the
+ * difference); the paper's one-sided READ carries the
+ * payload instead of the one-sided WRITE (reading R24).  Bind the
+ * producers' mirrors on this ring_t (ring_bind_mirror).  RING_EINVAL for
+ * RING_CREATE_LOCAL / fault-tolerant / reserve-then-commit rings.
+ * ring_destroy of an opened ring releases the mapping only. */
+ring_status_t ring_open(const ring_handle_t* handle, int device, ring_t* out);
 ring_status_t ring_get_info(ring_t ring, ring_info_t* out);
 /* Export a handle for producers in other processes (CUDA IPC) or this process. */
 ring_status_t ring_export(ring_t ring, ring_handle_t* out);

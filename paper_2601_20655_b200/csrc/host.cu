@@ -183,6 +183,8 @@ struct ring_s {
   uint32_t copy_ctas = 0, threads = 0, chunk = 0;
   const uint32_t* crc = nullptr;
   uint32_t sys = 1;
+  bool owner = true;                         // false: ring_open of a ring owned elsewhere (pull placement)
+  bool ipc_opened = false;                   // base is an IPC mapping of another process's ring
 };
 
 struct ring_peer_s {
@@ -416,8 +418,64 @@ ring_status_t ring_destroy(ring_t r) {
   for (void* p : r->opened) cudaIpcCloseMemHandle(p);
   cudaFree(r->ctx);
   cudaFree(r->mirrors_dev);
-  cudaFree(r->base);
+  if (r->owner) cudaFree(r->base);
+  else if (r->ipc_opened) cudaIpcCloseMemHandle(r->base);
   delete r;
+  return RING_OK;
+}
+
+// Pull placement: the consumer on `device` takes a ring that lives in another
+// GPU's memory (created there with ring_create, usually by its producer).  The
+// protocol is unchanged -- same words, same steps, same oracle -- only the
+// placement of the ring moves: the producer's WB becomes a local HBM write and
+// the consumer's copy-out get reads the payload over NVLink (the paper's
+// one-sided READ, in place of the one-sided WRITE).
+ring_status_t ring_open(const ring_handle_t* h, int device, ring_t* out) {
+  if (!h || !out) return RING_EINVAL;
+  HandleBlob b;
+  memcpy(&b, h->bytes, sizeof b);
+  if (b.magic != kMagicRing) return RING_EINVAL;
+  if (b.flags & (RING_CREATE_LOCAL | RING_CREATE_FAULT_TOLERANT | RING_CREATE_RESERVE_COMMIT)) return RING_EINVAL;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return RING_EINVAL;
+  const bool same_process = b.pid == (int32_t)getpid() && b.token == g_token;
+  ring_s* r = new ring_s;
+  r->device = device;
+  r->R = b.R;
+  r->N = b.N;
+  r->max_producers = b.max_producers;
+  r->flags = b.flags;
+  r->sys = 1;
+  r->owner = false;
+  r->data_off = data_offset(b.N);
+  r->alloc = r->data_off + b.R;
+  if (same_process) {
+    ring_status_t s = enable_peer(device, b.device);
+    if (s != RING_OK) { delete r; return s; }
+    r->base = reinterpret_cast<uint8_t*>(b.ptr);
+  } else {
+    DevGuard g(device);
+    void* m = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&m, b.ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      snprintf(g_cuda_err, sizeof g_cuda_err, "cudaIpcOpenMemHandle(ring): %s", cudaGetErrorString(e));
+      cudaGetLastError();
+      delete r;
+      return RING_EPEER;
+    }
+    r->base = static_cast<uint8_t*>(m);
+    r->ipc_opened = true;
+  }
+  DevGuard g(device);
+  CUDA_TRY(cudaMalloc(&r->mirrors_dev, sizeof(uint64_t*) * r->max_producers));
+  CUDA_TRY(cudaMemset(r->mirrors_dev, 0, sizeof(uint64_t*) * r->max_producers));
+  CUDA_TRY(cudaMalloc(&r->ctx, sizeof(LaunchCtx)));
+  CUDA_TRY(cudaMemset(r->ctx, 0, sizeof(LaunchCtx)));
+  CUDA_TRY(quiesce());
+  ring_status_t s = crc_table_dev(device, &r->crc);
+  if (s != RING_OK) return s;
+  *out = r;
   return RING_OK;
 }
 

@@ -77,6 +77,7 @@ def _load():
     P, U32, U64, I = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
     sig = {
         "ring_create": [I, U64, U32, U32, U32, C.POINTER(P)],
+        "ring_open": [C.POINTER(ring_handle_t), I, C.POINTER(P)],
         "ring_destroy": [P],
         "ring_get_info": [P, C.POINTER(ring_info_t)],
         "ring_export": [P, C.POINTER(ring_handle_t)],
@@ -163,6 +164,13 @@ def _ptr(x) -> int | None:
 def ring_create(device: int, data_bytes: int, n_slots: int, max_producers: int = 1, flags: int = 0) -> int:
     out = C.c_void_p()
     _check("ring_create", lib.ring_create(device, data_bytes, n_slots, max_producers, flags, C.byref(out)))
+    return out.value
+
+
+def ring_open(handle: bytes, device: int) -> int:
+    """Consumer side of a ring living in another GPU's memory (pull placement)."""
+    out = C.c_void_p()
+    _check("ring_open", lib.ring_open(C.byref(_handle(handle)), device, C.byref(out)))
     return out.value
 
 
