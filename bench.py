@@ -516,8 +516,8 @@ def bench_c2(args):
                                    "two kernels on this GPU (ring_probe_rtt, system scope)"},
         "kernels_ms": {"put_avg": round(put_avg_ms, 5), "consume_avg": round(statistics.mean(get_ms), 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("ncu_put_c2.json"),
-                     "traffic_source": "profiles/ncu_put_c2.json (ncu --set full, put_kernel, same config)",
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("r02_ncu_put_c2.json"),
+                     "traffic_source": "profiles/r02_ncu_put_c2.json (ncu --set full, put_kernel, same config)",
                      "kernel": "put_kernel<0> (persistent engine: time per batch = step time)" if engine
                      else "put_kernel<0> (CUDA-event average per launch)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src_kind})",
