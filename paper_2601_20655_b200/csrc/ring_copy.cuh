@@ -102,8 +102,14 @@ __device__ __forceinline__ uint64_t wait_planned(LaunchSet* S, CopyShared* cs, u
     const uint64_t v = ld_acquire_cta_shared64(&cs->pl);
     if (planned_units(v) > u || planned_done(v)) return v;
     if (atomicCAS_block(&cs->owner, 0u, 1u) == 0u) {
-      const uint64_t g = ld_acquire<false>(&S->planned);
-      if (g != v) st_release_cta_shared64(&cs->pl, g);   // monotonic: one poller at a time
+      // relaxed polls, one acquire fence when the word has moved: an
+      // ld.acquire invalidates the SM's L1 (CCTL.IVALL) on every poll, and
+      // the L1 stages the in-flight loads of the copy warps still working
+      uint64_t g = ld_relaxed<false>(&S->planned);
+      if (g != v) {
+        fence_acq_rel<false>();
+        st_release_cta_shared64(&cs->pl, g);              // monotonic: one poller at a time
+      }
       atomicExch_block(&cs->owner, 0u);
       if (planned_units(g) > u || planned_done(g)) return g;
     }
