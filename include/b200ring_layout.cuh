@@ -136,6 +136,14 @@ __device__ __forceinline__ int4 ld_stream16(const void* p) {
                : "l"(p));
   return v;
 }
+// Coherent 16-byte load (L2, never the non-coherent path): for memory another
+// agent writes while the kernel runs -- the consumer reading ring entries
+// (in its own HBM, or over NVLink with pull placement).
+__device__ __forceinline__ int4 ld_cg16(const void* p) {
+  int4 v;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void st16(void* p, int4 v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }

@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
     }
   }
   if (blockIdx.x != 0) __syncthreads();
-  if (a.dst) copy_warp(ctx, S, &cs, a.chunk, a.timeout_ns);
+  if (a.dst) copy_warp<3>(ctx, S, &cs, a.chunk, a.timeout_ns);
 }
 
 // In-order release of `count` received entries plus the PAD entries the read

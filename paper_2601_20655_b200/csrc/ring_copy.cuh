@@ -23,6 +23,9 @@ __device__ __forceinline__ uint32_t ld_cg32(const uint32_t* p) { return __ldcg(p
 __device__ __forceinline__ uint64_t ld_cg64(const uint64_t* p) { return __ldcg(reinterpret_cast<const unsigned long long*>(p)); }
 
 // Warp copy of `nb` bytes, lanes striding 16 B.
+// V = 3: coherent 16-B loads (ld.global.cg) -- the consumer's copy-out reads
+// ring entries that producers write while it runs (the non-coherent .nc path
+// is only for data read-only during the kernel: the put's sources).
 // V = 2: 32-B accesses (LDG/STG.256) when both sides are 32-B aligned
 // (payloads start 64 B into a 128-B aligned entry, so whenever the source is):
 // +1.5 % over NVLink, but -12 % for HBM -> HBM (C2), so only the put kernel
@@ -44,7 +47,7 @@ __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8
       for (int j = 0; j < U; ++j) st32(dst + 32ull * (i + j * 32), v[j]);
     }
     for (; i < n32; i += 32) st32(dst + 32ull * i, ld_stream32(src + 32ull * i));
-    for (uint64_t j = ((uint64_t)n32 << 5) + lane; j < nb; j += 32) dst[j] = src[j];
+    for (uint64_t j = ((uint64_t)n32 << 5) + lane; j < nb; j += 32) dst[j] = V == 3 ? __ldcg(src + j) : src[j];
   } else if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
     const int4* s = reinterpret_cast<const int4*>(src);
     int4* d = reinterpret_cast<int4*>(dst);
@@ -54,20 +57,20 @@ __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8
     for (; i + (U - 1) * 32 < n16; i += U * 32) {
       int4 v[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) v[j] = ld_stream16(s + i + j * 32);
+      for (int j = 0; j < U; ++j) v[j] = V == 3 ? ld_cg16(s + i + j * 32) : ld_stream16(s + i + j * 32);
 #pragma unroll
       for (int j = 0; j < U; ++j) st16(d + i + j * 32, v[j]);
     }
-    for (; i < n16; i += 32) st16(d + i, ld_stream16(s + i));
-    for (uint64_t j = ((uint64_t)n16 << 4) + lane; j < nb; j += 32) dst[j] = src[j];
+    for (; i < n16; i += 32) st16(d + i, V == 3 ? ld_cg16(s + i) : ld_stream16(s + i));
+    for (uint64_t j = ((uint64_t)n16 << 4) + lane; j < nb; j += 32) dst[j] = V == 3 ? __ldcg(src + j) : src[j];
   } else if ((((uintptr_t)src | (uintptr_t)dst) & 3) == 0) {
     const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
     uint32_t* d = reinterpret_cast<uint32_t*>(dst);
     const uint64_t n4 = nb >> 2;
-    for (uint64_t i = lane; i < n4; i += 32) d[i] = s[i];
-    for (uint64_t j = (n4 << 2) + lane; j < nb; j += 32) dst[j] = src[j];
+    for (uint64_t i = lane; i < n4; i += 32) d[i] = V == 3 ? __ldcg(s + i) : s[i];
+    for (uint64_t j = (n4 << 2) + lane; j < nb; j += 32) dst[j] = V == 3 ? __ldcg(src + j) : src[j];
   } else {
-    for (uint64_t j = lane; j < nb; j += 32) dst[j] = src[j];
+    for (uint64_t j = lane; j < nb; j += 32) dst[j] = V == 3 ? __ldcg(src + j) : src[j];
   }
 }
 
