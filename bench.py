@@ -547,7 +547,23 @@ def bench_pairs(args, rank, world, grp):
     m = args.msgs_per_step or 32
     pull = bool(args.pull)
     own = None
-    if pull:
+    if args.pull == 2:
+        # split placement: the ring's control words + header copies on this rank,
+        # its buffer region on the previous rank's GPU (the producer writes
+        # locally, this rank pulls each payload over NVLink)
+        prev, nxt = (rank - 1) % world, (rank + 1) % world
+        ndev = torch.cuda.device_count()
+        ring = R.ring_create_split(dev, (dev - 1) % ndev, Rb, N, 1, 0)
+        hs = [None] * world
+        dist.all_gather_object(hs, R.ring_export(ring), group=grp)
+        peer, mh = R.ring_attach_peer(hs[nxt], dev, 0)
+        mhs = [None] * world
+        dist.all_gather_object(mhs, mh, group=grp)
+        R.ring_bind_mirror(ring, 0, mhs[prev])
+        if args.cons_ctas or args.cons_threads:
+            R.ring_config(ring, args.cons_ctas, args.cons_threads)
+        dist.barrier(group=grp)
+    elif pull:
         # pull placement: each rank's egress ring lives in its OWN memory; the
         # next rank opens it and pulls every payload over NVLink (ring_open)
         own = R.ring_create(dev, Rb, N, 1, 0)
@@ -703,7 +719,11 @@ def bench_pairs(args, rank, world, grp):
         cpu = cpu_baseline(Rb, N, 1, 500, C3_LENS[1], C3_LENS[0], args.cpu_budget,
                            "C3 shape: U[4,193,280, 4,194,304]-B payloads")
     dist.barrier(group=grp)
-    if pull:
+    if args.pull == 2:
+        R.ring_detach(peer)
+        dist.barrier(group=grp)
+        R.ring_destroy(ring)
+    elif pull:
         R.ring_destroy(ring)            # the mapping of the previous rank's ring
         dist.barrier(group=grp)
         R.ring_detach(peer)
@@ -725,11 +745,15 @@ def bench_pairs(args, rank, world, grp):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": ("C3-shaped ring of pairs, PULL placement: rank r's egress ring lives on rank r, rank "
+        "config": {"workload": ("C3-shaped ring of pairs, SPLIT placement: control words + header copies at the "
+                                "consumer, buffer region at the producer, payloads pulled over NVLink (copy-out)"
+                                if args.pull == 2 else
+                                "C3-shaped ring of pairs, PULL placement: rank r's egress ring lives on rank r, rank "
                                 "(r+1)%N opens it and pulls every payload over NVLink (copy-out consume)" if pull else
                                 "C3-shaped ring of pairs: rank r -> ring on rank (r+1)%N over NVLink") +
                                ", Wan2.1 umT5 emb 512x4096 bf16 / 480p latent 16x21x60x104 bf16 alternating",
-                   "placement": "pull (ring_open)" if pull else "push (ring at the consumer)",
+                   "placement": {0: "push (ring at the consumer)", 1: "pull (ring_open)",
+                                 2: "split (ring_create_split)"}[args.pull],
                    "R_bytes": Rb, "n_slots": N, "msgs_per_step_per_rank": m,
                    "l2": "inputs larger than L2 per rank (2 x 128 MiB source sets)",
                    "parallelism": f"{world} concurrent SPSC rings (one egress + one ingress stream per GPU)"},
@@ -871,7 +895,8 @@ def main():
     ap.add_argument("--cons-ctas", type=int, default=0, help="N>1 pull: consumer copy-out grid (0 = default)")
     ap.add_argument("--cons-threads", type=int, default=0)
     ap.add_argument("--pull", type=int, default=0,
-                    help="N>1 pairs: 1 = pull placement (ring at the producer, consumer pulls over NVLink)")
+                    help="N>1 pairs: 1 = pull placement (ring at the producer, consumer pulls over NVLink), "
+                         "2 = split placement (control at the consumer, buffer region at the producer)")
     ap.add_argument("--engine", type=int, default=0,
                     help="N=1: 1 = persistent put engine (doorbells), 0 = one put launch per step")
     ap.add_argument("--graph", action="store_true",

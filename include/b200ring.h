@@ -105,9 +105,9 @@ typedef struct ring_peer_s* ring_peer_t; /* producer side; BORROWS a mapping of 
 typedef struct router_s* router_t;       /* stage router (NodeManager / ResultDeliver stand-in) */
 
 /* Opaque, position-independent handle exchanged between processes (e.g. with a
- * torch.distributed all_gather of 128-byte tensors).  Carries a CUDA IPC memory
- * handle plus the ring geometry. */
-typedef struct { unsigned char bytes[128]; } ring_handle_t;
+ * torch.distributed all_gather of 256-byte tensors).  Carries the CUDA IPC memory
+ * handle(s) plus the ring geometry. */
+typedef struct { unsigned char bytes[256]; } ring_handle_t;
 
 /* User-supplied header fields of a workflow message (UUID
  * assigned by the proxy, proxy timestamp, application ID, stage). 32 bytes. */
@@ -166,6 +166,20 @@ ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uin
                           uint32_t flags, ring_t* out);
 /* Free the ring.  All peers must be detached first (their mappings are borrowed). */
 ring_status_t ring_destroy(ring_t ring);
+/* ring_create_split: split placement (reading R28).  The control
+ * words, the size slots and a copy of every entry header stay on the
+ * consumer's `device` (polled and read locally, as in the paper's layout); the
+ * buffer region of R bytes is allocated on `data_device` -- the producer's GPU.
+ * The producer writes each entry (header + payload) into its local HBM and
+ * the header, size slot and tail into the consumer's control region; the
+ * consumer's copy-out get pulls the payload over NVLink (the paper's one-sided
+ * READ).  Same protocol, placements and oracle as ring_create; only the
+ * memory the buffer region lives in changes.  Producers attach with
+ * ring_attach_peer as usual (from any process; the handle carries both
+ * allocations).  RING_EINVAL with RING_CREATE_LOCAL, FAULT_TOLERANT or
+ * RESERVE_COMMIT; fused device puts (ring_peer_device_view) are refused. */
+ring_status_t ring_create_split(int device, int data_device, uint64_t data_bytes, uint32_t n_slots,
+                                uint32_t max_producers, uint32_t flags, ring_t* out);
 /* ring_open: the consumer side of a ring that lives in ANOTHER GPU's memory
  * (pull placement).  The ring is created (and destroyed, after every ring_open
  * of it) on the producer's GPU, its producers attach there as usual; the

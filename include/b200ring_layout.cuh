@@ -41,6 +41,14 @@ constexpr int kMaxRouterDests = 32;   // destinations per launch (bit mask)
 __host__ __device__ inline uint64_t data_offset(uint32_t n_slots) {
   return (kSlotsOff + 8ull * n_slots + 4095ull) & ~4095ull;
 }
+// Split placement (ring_create_split): a copy of each entry header, indexed by
+// slot, follows the size region in the consumer's control allocation.
+__host__ __device__ inline uint64_t hdr_mirror_offset(uint32_t n_slots) {
+  return (kSlotsOff + 8ull * n_slots + 127) / 128 * 128;
+}
+__host__ __device__ inline uint64_t split_control_bytes(uint32_t n_slots) {
+  return (hdr_mirror_offset(n_slots) + 64ull * n_slots + 4095) / 4096 * 4096;
+}
 // f = align_up(64 + len, 128)  (R9)
 __host__ __device__ inline uint64_t footprint(uint64_t len) { return (kHdr + len + kAlign - 1) & ~(kAlign - 1); }
 // P_b update, PAPER.md:731-739 (strict '<': exact fit wraps to 0)

@@ -109,7 +109,8 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
     bool deliver = false;
     uint32_t hw[16] = {};
     if (in && ismsg) {
-      const int4* hp = reinterpret_cast<const int4*>(a.data + start);
+      const int4* hp = reinterpret_cast<const int4*>(
+          a.hdrs ? a.hdrs + 64ull * ((ptr_seq(G) + lane) & (a.N - 1)) : a.data + start);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int4 v = __ldcg(hp + q);

@@ -45,6 +45,11 @@ struct HandleBlob {
   uint32_t flags;
   uint32_t producer_id;  // mirror handles
   cudaIpcMemHandle_t ipc;
+  // split placement (ring_create_split): the buffer region is a second allocation
+  uint64_t data_ptr;     // 0 = the buffer region follows the control words in `ptr`
+  int32_t data_device;
+  uint32_t _d;
+  cudaIpcMemHandle_t data_ipc;
 };
 static_assert(sizeof(HandleBlob) <= sizeof(ring_handle_t), "handle too large");
 
@@ -185,11 +190,15 @@ struct ring_s {
   uint32_t sys = 1;
   bool owner = true;                         // false: ring_open of a ring owned elsewhere (pull placement)
   bool ipc_opened = false;                   // base is an IPC mapping of another process's ring
+  uint8_t* data = nullptr;                   // buffer region (base + data_off, or the split allocation)
+  uint8_t* hdrs = nullptr;                   // split placement: header copies in the control allocation
+  int data_device = -1;                      // split placement: the GPU holding the buffer region
 };
 
 struct ring_peer_s {
   int device = 0;
   int ring_device = 0;
+  int data_device = 0;                       // where the buffer region lives (the ring's GPU unless split)
   uint8_t* ring = nullptr;
   bool ipc_opened = false;
   DestState* st = nullptr;
@@ -201,6 +210,7 @@ struct ring_peer_s {
   uint32_t copy_ctas = 0, threads = 0, chunk = 0, copy_mode = 0;
   uint64_t* trace = nullptr;                 // debug timeline (B200RING_TRACE=1)
   const uint32_t* crc = nullptr;
+  uint8_t* data_opened = nullptr;            // split placement: IPC mapping of the buffer region
   FaultSpec fault;                           // test-only fault injection (fault-tolerant rings)
   void* stage_ctl = nullptr;                 // grid-coordination block of fused puts (ring_stage.cuh)
   uint32_t launches_stage = 0;
@@ -392,6 +402,7 @@ ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uin
   r->data_off = data_offset(n_slots);
   r->alloc = r->data_off + data_bytes;
   cudaError_t e = cudaMalloc(&r->base, r->alloc);
+  r->data = r->base + r->data_off;
   if (e != cudaSuccess) {
     cudaGetLastError();
     delete r;
@@ -411,6 +422,56 @@ ring_status_t ring_create(int device, uint64_t data_bytes, uint32_t n_slots, uin
   return RING_OK;
 }
 
+ring_status_t ring_create_split(int device, int data_device, uint64_t data_bytes, uint32_t n_slots,
+                                uint32_t max_producers, uint32_t flags, ring_t* out) {
+  if (!out || data_bytes == 0 || data_bytes % kAlign || data_bytes >= (1ull << 39) || n_slots == 0 ||
+      (n_slots & (n_slots - 1)) || n_slots > RING_MAX_SLOTS || max_producers == 0 ||
+      max_producers > RING_MAX_PRODUCERS ||
+      (flags & (RING_CREATE_LOCAL | RING_CREATE_FAULT_TOLERANT | RING_CREATE_RESERVE_COMMIT)))
+    return RING_EINVAL;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev || data_device < 0 || data_device >= ndev) return RING_EINVAL;
+  ring_status_t s = enable_peer(device, data_device);
+  if (s == RING_OK) s = enable_peer(data_device, device);
+  if (s != RING_OK) return s;
+  ring_s* r = new ring_s;
+  r->device = device;
+  r->data_device = data_device;
+  r->R = data_bytes;
+  r->N = n_slots;
+  r->max_producers = max_producers;
+  r->flags = flags;
+  r->sys = 1;
+  r->data_off = split_control_bytes(n_slots);   // (ring_get_info: no buffer region in this allocation)
+  r->alloc = r->data_off;
+  {
+    DevGuard gd(data_device);
+    cudaError_t e = cudaMalloc(&r->data, data_bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); delete r; return RING_ENOMEM; }
+  }
+  DevGuard g(device);
+  cudaError_t e = cudaMalloc(&r->base, r->alloc);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    DevGuard gd(data_device);
+    cudaFree(r->data);
+    delete r;
+    return RING_ENOMEM;
+  }
+  r->hdrs = r->base + hdr_mirror_offset(n_slots);
+  CUDA_TRY(cudaMemset(r->base, 0, r->alloc));
+  CUDA_TRY(cudaMalloc(&r->mirrors_dev, sizeof(uint64_t*) * max_producers));
+  CUDA_TRY(cudaMemset(r->mirrors_dev, 0, sizeof(uint64_t*) * max_producers));
+  CUDA_TRY(cudaMalloc(&r->ctx, sizeof(LaunchCtx)));
+  CUDA_TRY(cudaMemset(r->ctx, 0, sizeof(LaunchCtx)));
+  CUDA_TRY(quiesce());
+  s = crc_table_dev(device, &r->crc);
+  if (s != RING_OK) return s;
+  *out = r;
+  return RING_OK;
+}
+
 ring_status_t ring_destroy(ring_t r) {
   if (!r) return RING_EINVAL;
   DevGuard g(r->device);
@@ -420,6 +481,10 @@ ring_status_t ring_destroy(ring_t r) {
   cudaFree(r->mirrors_dev);
   if (r->owner) cudaFree(r->base);
   else if (r->ipc_opened) cudaIpcCloseMemHandle(r->base);
+  if (r->owner && r->data_device >= 0) {
+    DevGuard gd(r->data_device);
+    cudaFree(r->data);
+  }
   delete r;
   return RING_OK;
 }
@@ -448,6 +513,7 @@ ring_status_t ring_open(const ring_handle_t* h, int device, ring_t* out) {
   r->flags = b.flags;
   r->sys = 1;
   r->owner = false;
+  if (b.data_ptr) { delete r; return RING_EINVAL; }   // split rings are consumed where their control words live
   r->data_off = data_offset(b.N);
   r->alloc = r->data_off + b.R;
   if (same_process) {
@@ -467,6 +533,7 @@ ring_status_t ring_open(const ring_handle_t* h, int device, ring_t* out) {
     r->base = static_cast<uint8_t*>(m);
     r->ipc_opened = true;
   }
+  r->data = r->base + r->data_off;
   DevGuard g(device);
   CUDA_TRY(cudaMalloc(&r->mirrors_dev, sizeof(uint64_t*) * r->max_producers));
   CUDA_TRY(cudaMemset(r->mirrors_dev, 0, sizeof(uint64_t*) * r->max_producers));
@@ -486,7 +553,7 @@ ring_status_t ring_get_info(ring_t r, ring_info_t* out) {
   out->max_producers = r->max_producers;
   out->data_bytes = r->R;
   out->base = reinterpret_cast<uint64_t>(r->base);
-  out->data = reinterpret_cast<uint64_t>(r->base + r->data_off);
+  out->data = reinterpret_cast<uint64_t>(r->data);
   out->data_offset = r->data_off;
   out->alloc_bytes = r->alloc;
   return RING_OK;
@@ -506,6 +573,12 @@ ring_status_t ring_export(ring_t r, ring_handle_t* out) {
   b.flags = r->flags;
   DevGuard g(r->device);
   CUDA_TRY(cudaIpcGetMemHandle(&b.ipc, r->base));
+  if (r->data_device >= 0) {
+    b.data_ptr = reinterpret_cast<uint64_t>(r->data);
+    b.data_device = r->data_device;
+    DevGuard gd(r->data_device);
+    CUDA_TRY(cudaIpcGetMemHandle(&b.data_ipc, r->data));
+  }
   memset(out, 0, sizeof *out);
   memcpy(out->bytes, &b, sizeof b);
   return RING_OK;
@@ -525,6 +598,7 @@ ring_status_t ring_attach_peer(const ring_handle_t* h, int producer_device, uint
   ring_peer_s* p = new ring_peer_s;
   p->device = producer_device;
   p->ring_device = b.device;
+  p->data_device = b.data_ptr ? b.data_device : b.device;
   if (same_process) {
     ring_status_t s = enable_peer(producer_device, b.device);
     if (s != RING_OK) { delete p; return s; }
@@ -553,6 +627,25 @@ ring_status_t ring_attach_peer(const ring_handle_t* h, int producer_device, uint
   CUDA_TRY(cudaMemset(p->ctx, 0, sizeof(LaunchCtx)));
   p->desc.ring = p->ring;
   p->desc.data = p->ring + data_offset(b.N);
+  if (b.data_ptr) {   // split placement: the buffer region is its own allocation (usually on this GPU)
+    if (same_process) {
+      ring_status_t s2 = enable_peer(producer_device, b.data_device);
+      if (s2 != RING_OK) return s2;
+      p->desc.data = reinterpret_cast<uint8_t*>(b.data_ptr);
+    } else {
+      DevGuard gd(producer_device);
+      void* m = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&m, b.data_ipc, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        snprintf(g_cuda_err, sizeof g_cuda_err, "cudaIpcOpenMemHandle(data): %s", cudaGetErrorString(e));
+        cudaGetLastError();
+        return RING_EPEER;
+      }
+      p->data_opened = static_cast<uint8_t*>(m);
+      p->desc.data = p->data_opened;
+    }
+    p->desc.hdrs = p->ring + hdr_mirror_offset(b.N);
+  }
   p->desc.st = p->st;
   p->desc.R = b.R;
   p->desc.N = b.N;
@@ -631,6 +724,7 @@ ring_status_t ring_detach(ring_peer_t p) {
   if (p->eng_ready) cudaEventDestroy(p->eng_ready);
   if (p->eng_stream) cudaStreamDestroy(p->eng_stream);
   if (p->ipc_opened) cudaIpcCloseMemHandle(p->ring);
+  if (p->data_opened) cudaIpcCloseMemHandle(p->data_opened);
   cudaFree(p->desc_dev);
   cudaFree(p->ctx);
   cudaFree(p->st);
@@ -677,7 +771,7 @@ ring_status_t ring_set_create(const ring_t* rings, uint32_t n, ring_set_t* out) 
   for (uint32_t i = 0; i < n; ++i) {
     ring_t r = rings[i];
     if (!r || r->device != rings[0]->device) return RING_EINVAL;
-    h[i] = SetRingHost{r->base, r->base + r->data_off, r->mirrors_dev, r->R, r->N, 0};
+    h[i] = SetRingHost{r->base, r->data, r->mirrors_dev, r->R, r->N, 0};
   }
   ring_set_s* s = new ring_set_s;
   s->device = rings[0]->device;
@@ -713,7 +807,7 @@ ring_status_t ring_set_consume(ring_set_t s, uint32_t n, ring_view_t* d_views, u
 }
 
 ring_status_t ring_peer_device_view(ring_peer_t p, ring_dev_peer_t* out) {
-  if (!p || !out || p->desc.mpsc || p->engine_on) return RING_EINVAL;
+  if (!p || !out || p->desc.mpsc || p->engine_on || p->desc.hdrs) return RING_EINVAL;
   DevGuard g(p->device);
   if (!p->stage_ctl) {
     CUDA_TRY(cudaMalloc(&p->stage_ctl, sizeof(stage::StageCtl)));
@@ -858,7 +952,7 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   a.flags = flags;
   uint32_t ctas = p->copy_ctas, thr = p->threads, chunk = p->chunk;
   DevGuard g(p->device);
-  default_grid(p->device, p->device != p->ring_device, &ctas, &thr, &chunk);
+  default_grid(p->device, p->device != p->data_device, &ctas, &thr, &chunk);
   a.copy_mode = p->copy_mode;
   // engine stages live in shared memory: the largest power of two that fits
   while (a.copy_mode == 1 && chunk > 4096 && (uint64_t)chunk * kEngineStages > kEngineSmem) chunk >>= 1;
@@ -922,14 +1016,14 @@ static ring_status_t engine_launch(ring_peer_t p, void* stream) {
     CUDA_TRY(cudaMemsetAsync(a.trace, 0, kTraceWords * 8, p->eng_stream));
   }
   uint32_t ctas = p->copy_ctas, thr = p->threads, chunk = p->chunk;
-  if (!ctas && p->device == p->ring_device) {
+  if (!ctas && p->device == p->data_device) {
     // a resident grid on every SM would leave no SM for kernels with another
     // shared-memory split (they only start next to CTAs of the same split)
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
     ctas = (uint32_t)std::max(1, nsm - 8);
   }
-  default_grid(p->device, p->device != p->ring_device, &ctas, &thr, &chunk);
+  default_grid(p->device, p->device != p->data_device, &ctas, &thr, &chunk);
   a.chunk = chunk;
   a.launch = p->launches;
   CUDA_TRY(launch_put(a, ctas, thr, p->eng_stream));
@@ -1018,7 +1112,8 @@ static ring_status_t get_common(ring_t r, uint32_t n, ring_view_t* d_views, void
   if (!r || !d_views || n == 0 || (d_dst && dst_stride == 0)) return RING_EINVAL;
   GetArgs a{};
   a.ring = r->base;
-  a.data = r->base + r->data_off;
+  a.data = r->data;
+  a.hdrs = r->hdrs;
   a.views = d_views;
   a.dst = static_cast<uint8_t*>(d_dst);
   a.mirrors = r->mirrors_dev;
@@ -1092,7 +1187,7 @@ ring_status_t ring_read_data(ring_t r, uint64_t offset, uint64_t len, void* host
   if (!r || (len && !host_dst) || offset > r->R || len > r->R - offset) return RING_EINVAL;
   DevGuard g(r->device);
   CUDA_TRY(quiesce());
-  if (len) CUDA_TRY(cudaMemcpy(host_dst, r->base + r->data_off + offset, len, cudaMemcpyDeviceToHost));
+  if (len) CUDA_TRY(cudaMemcpy(host_dst, r->data + offset, len, cudaMemcpyDefault));
   return RING_OK;
 }
 
@@ -1100,7 +1195,7 @@ ring_status_t ring_write_data(ring_t r, uint64_t offset, uint64_t len, const voi
   if (!r || (len && !host_src) || offset > r->R || len > r->R - offset) return RING_EINVAL;
   DevGuard g(r->device);
   CUDA_TRY(quiesce());
-  if (len) CUDA_TRY(cudaMemcpy(r->base + r->data_off + offset, host_src, len, cudaMemcpyHostToDevice));
+  if (len) CUDA_TRY(cudaMemcpy(r->data + offset, host_src, len, cudaMemcpyDefault));
   CUDA_TRY(quiesce());
   return RING_OK;
 }
@@ -1241,7 +1336,7 @@ ring_status_t ring_put_routed(router_t r, const ring_msg_t* d_msgs, uint32_t n, 
   a.n = n;
   a.flags = flags;
   bool remote = false;
-  for (auto* p : r->dests) remote = remote || p->ring_device != r->device;
+  for (auto* p : r->dests) remote = remote || p->data_device != r->device;
   uint32_t ctas = r->copy_ctas, thr = r->threads, chunk = r->chunk;
   DevGuard g(r->device);
   default_grid(r->device, remote, &ctas, &thr, &chunk);

@@ -946,6 +946,11 @@ __device__ __forceinline__ void write_header(const PutArgs& a, LaunchCtx* ctx, u
     RING_CHECK(ld_cg64(&p.start) + kHdr <= D.R, "header inside R", ld_cg64(&p.start), D.R);
 #pragma unroll
     for (int q = 0; q < 4; ++q) st16(hd + 16 * q, make_int4((int)w[4 * q], (int)w[4 * q + 1], (int)w[4 * q + 2], (int)w[4 * q + 3]));
+    if (D.hdrs) {   // split placement: the consumer reads the header from its own memory
+      uint8_t* hm = D.hdrs + 64ull * (ld_cg32(&p.slot) & (D.N - 1));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) st16(hm + 16 * q, make_int4((int)w[4 * q], (int)w[4 * q + 1], (int)w[4 * q + 2], (int)w[4 * q + 3]));
+    }
   }
   if (!D.mpsc) {   // WL (SPSC, early; PAD entries carry the pad bit)
     if (D.sys) st_relaxed<true>(slot_w(D, ld_cg32(&p.slot)), ld_cg64(&p.slot_word));

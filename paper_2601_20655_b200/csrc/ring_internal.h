@@ -45,6 +45,7 @@ struct DestDesc {
   uint32_t ft;           // RING_CREATE_FAULT_TOLERANT: take-over, CAS WL/UH/Unlock, tags, payload CRC
   uint32_t rc;           // RING_CREATE_RESERVE_COMMIT: claim under the lock, copy and commit outside it
   uint32_t _pad2;
+  uint8_t* hdrs;         // split placement: the consumer's header copies (slot-indexed, 64 B each), else null
 };
 
 // Test-only fault injection of a put launch (ring_peer_set_fault).
@@ -242,6 +243,7 @@ constexpr uint32_t kEngineSmem = 200u << 10;             // dynamic shared memor
 struct GetArgs {
   uint8_t* ring;
   uint8_t* data;
+  const uint8_t* hdrs;  // split placement: local header copies (slot-indexed), else null: headers at data + start
   ring_view_t* views;
   uint8_t* dst;
   uint64_t** mirrors;   // device array of mirror word pointers (consumer address space)

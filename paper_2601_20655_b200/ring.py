@@ -34,7 +34,7 @@ class ring_hdr_t(C.Structure):
 
 
 class ring_handle_t(C.Structure):
-    _fields_ = [("bytes", C.c_ubyte * 128)]
+    _fields_ = [("bytes", C.c_ubyte * 256)]
 
 
 class ring_fault_t(C.Structure):
@@ -77,6 +77,7 @@ def _load():
     P, U32, U64, I = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
     sig = {
         "ring_create": [I, U64, U32, U32, U32, C.POINTER(P)],
+        "ring_create_split": [I, I, U64, U32, U32, U32, C.POINTER(P)],
         "ring_open": [C.POINTER(ring_handle_t), I, C.POINTER(P)],
         "ring_destroy": [P],
         "ring_get_info": [P, C.POINTER(ring_info_t)],
@@ -167,6 +168,16 @@ def ring_create(device: int, data_bytes: int, n_slots: int, max_producers: int =
     return out.value
 
 
+def ring_create_split(device: int, data_device: int, data_bytes: int, n_slots: int, max_producers: int = 1,
+                      flags: int = 0) -> int:
+    """Split placement: control words + header copies on `device` (the consumer),
+    the buffer region on `data_device` (the producer's GPU)."""
+    out = C.c_void_p()
+    _check("ring_create_split", lib.ring_create_split(device, data_device, data_bytes, n_slots, max_producers, flags,
+                                                      C.byref(out)))
+    return out.value
+
+
 def ring_open(handle: bytes, device: int) -> int:
     """Consumer side of a ring living in another GPU's memory (pull placement)."""
     out = C.c_void_p()
@@ -192,7 +203,7 @@ def ring_export(ring: int) -> bytes:
 
 def _handle(b: bytes) -> ring_handle_t:
     h = ring_handle_t()
-    C.memmove(h.bytes, bytes(b), 128)
+    C.memmove(h.bytes, bytes(b), 256)
     return h
 
 

@@ -5,7 +5,7 @@ Every hop between two stages is one ring owned by the consuming GPU
 decides which rings each rank creates, which rings it attaches to as a
 producer (and with which producer id), and whose head mirrors it binds, for
 the BASELINE.json topologies, and performs the handle exchange over a
-torch.distributed group (an all_gather of 128-byte handles -- the RDMA
+torch.distributed group (an all_gather of 256-byte handles -- the RDMA
 queue-pair / registered-address setup of PAPER.md:637-641; never on the data
 path).  The ring calls are injected, so the wiring itself is testable on CPU
 with a gloo group.

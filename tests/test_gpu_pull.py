@@ -153,3 +153,72 @@ def test_open_rejects_local_rings(R):
             R.ring_open(R.ring_export(owner), 0)
     finally:
         R.ring_destroy(owner)
+
+
+# ---------------------------------------------------------------------------------------
+# split placement (ring_create_split): control words + header copies at the
+# consumer, the buffer region at the producer
+# ---------------------------------------------------------------------------------------
+def _split_stream(R, L, stream, prod, cons, cap):
+    ring = R.ring_create_split(cons, prod, L.R, L.N, 1, 0)
+    peer, mh = R.ring_attach_peer(R.ring_export(ring), prod, 0)
+    R.ring_bind_mirror(ring, 0, mh)
+    buf, srcs = upload(stream, f"cuda:{prod}")
+    msgs = msg_tensor(stream, srcs, f"cuda:{prod}")
+    n = len(stream)
+    vt = torch.zeros(n * 128, dtype=torch.uint8, device=f"cuda:{cons}")
+    dst = torch.zeros(n * cap, dtype=torch.uint8, device=f"cuda:{cons}")
+    st = torch.full((n,), 10, dtype=torch.int32, device=f"cuda:{prod}")
+    sc, sp = torch.cuda.Stream(cons), torch.cuda.Stream(prod)
+    R.ring_consume(ring, n, vt, dst, cap, 0, sc)
+    R.ring_put_batch(peer, msgs, n, 0, st, sp)
+    torch.cuda.synchronize(prod)
+    torch.cuda.synchronize(cons)
+    v = views_host(vt)
+    d = dst.cpu().numpy()
+    pl = [d[j * cap: j * cap + int(v[j]["len"])].tobytes() for j in range(n)]
+    img = R.ring_read_image(ring)
+    status = st.cpu().tolist()
+    R.ring_detach(peer)
+    R.ring_destroy(ring)
+    return v, pl, status, img
+
+
+@CROSS
+def test_split_c3_wan_tensors(R, cross):
+    prod, cons = devices(2, cross)
+    L = Layout(64 << 20, 64)
+    stream = synth.wan_stream(synth.SEED_BASE + 3, 0, 48)
+    sim = oracle_spsc(L, to_oracle_msgs(stream))
+    v, pl, st, img = _split_stream(R, L, stream, prod, cons, 4194304)
+    assert st == [0] * 48, st
+    check_views_against_oracle(v, sim, 0, stream)
+    assert pl == [m.payload.tobytes() for m in stream]
+    assert img["tail"] == sim.mem.tail == img["head"]
+
+
+@CROSS
+def test_split_small_ring_many_laps(R, cross):
+    prod, cons = devices(2, cross)
+    L = Layout(32768, 8)
+    stream = synth.random_stream(synth.SEED_BASE + 1, 0, 1000, 1, 4096)
+    sim = oracle_spsc(L, to_oracle_msgs(stream))
+    v, pl, st, img = _split_stream(R, L, stream, prod, cons, 4096)
+    assert st == [0] * 1000
+    check_views_against_oracle(v, sim, 0, stream)
+    assert pl == [m.payload.tobytes() for m in stream]
+
+
+def test_split_rejects(R):
+    with pytest.raises(R.RingError):
+        R.ring_create_split(0, 0, 1 << 20, 8, 1, R.RING_CREATE_FAULT_TOLERANT)
+    ring = R.ring_create_split(0, 0, 1 << 20, 8, 1, 0)
+    peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
+    try:
+        with pytest.raises(R.RingError):
+            R.ring_peer_device_view(peer)        # a fused put would not write the header copies
+        with pytest.raises(R.RingError):
+            R.ring_open(R.ring_export(ring), 0)  # consumed where its control words live
+    finally:
+        R.ring_detach(peer)
+        R.ring_destroy(ring)
