@@ -405,7 +405,10 @@ ring_status_t ring_write_data(ring_t ring, uint64_t offset, uint64_t len, const 
  * A device-resident route table on the producer GPU: for each (app_id, stage)
  * a list of up to 8 destination attachments, a round-robin counter and an epoch.
  * router_set_route replaces the list and flips the epoch; puts already launched
- * finish to their old destination. */
+ * finish to their old destination.  The update is a one-thread
+ * kernel on `stream` (the route travels in its parameters): destinations
+ * first, the epoch last with a release -- no host synchronisation.  Attachments
+ * of fault-tolerant rings or with a running put engine are refused. */
 ring_status_t router_create(int device, uint32_t max_routes, router_t* out);
 ring_status_t router_destroy(router_t r);
 ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, const ring_peer_t* dests, uint32_t n,

@@ -1240,6 +1240,7 @@ ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, cons
   nr.app_id = app_id;
   nr.stage = stage;
   nr.n = (uint16_t)n;
+  std::vector<uint32_t> added;   // destinations new to this router: their descriptors go up first
   for (uint32_t i = 0; i < n; ++i) {
     ring_peer_t p = dests[i];
     // A routed put runs the batched (non-fault-tolerant) sender: it must never
@@ -1250,8 +1251,7 @@ ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, cons
     if (idx == r->dests.size()) {
       if (idx >= (uint32_t)kMaxRouterDests) return RING_EINVAL;
       r->dests.push_back(p);
-      CUDA_TRY(cudaMemcpyAsync(r->dests_dev + idx, &p->desc, sizeof(DestDesc), cudaMemcpyHostToDevice, as_stream(stream)));
-      CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+      added.push_back(idx);
     }
     nr.dests[i] = idx;
   }
@@ -1264,14 +1264,15 @@ ring_status_t router_set_route(router_t r, uint32_t app_id, uint16_t stage, cons
   if (slot == r->max_routes) return RING_EINVAL;
   nr.epoch = r->routes[slot].epoch + 1;     // epoch flip (NodeManager reassignment)
   r->routes[slot] = nr;
-  // Write everything but the device-owned rr counter, in stream order with the
-  // caller's puts: launched puts finish to the old destination.
-  static thread_local Route staged;
-  staged = nr;
+  // Device-side, in stream order with the caller's puts (launched puts finish
+  // to the old destinations), no host synchronisation.
   Route* d = r->routes_dev + slot;
-  CUDA_TRY(cudaMemcpyAsync(d, &staged, offsetof(Route, rr), cudaMemcpyHostToDevice, as_stream(stream)));
-  CUDA_TRY(cudaMemcpyAsync(&d->dests, &staged.dests, sizeof(staged.dests), cudaMemcpyHostToDevice, as_stream(stream)));
-  CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+  for (size_t k = 0; k + 1 < added.size(); ++k)
+    CUDA_TRY(launch_route_update(d, r->routes[slot], r->dests_dev + added[k], &r->dests[added[k]]->desc,
+                                 as_stream(stream)));
+  CUDA_TRY(launch_route_update(d, nr, added.empty() ? nullptr : r->dests_dev + added.back(),
+                               added.empty() ? nullptr : &r->dests[added.back()]->desc, as_stream(stream)));
+  g_launches += added.size() > 1 ? added.size() : 1;
   return RING_OK;
 }
 

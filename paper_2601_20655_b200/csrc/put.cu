@@ -1357,6 +1357,27 @@ __global__ void engine_wait_kernel(EngineQueue* q, uint64_t upto, uint64_t timeo
   }
 }
 
+// NodeManager reassignment (router_set_route), stream-ordered
+// and without a host round trip: the new route (and a new destination's
+// descriptor) travel in the kernel parameters; the destinations, the set size
+// and the app / stage are written first, the epoch last with a release -- the
+// device-side epoch flip a reader acquiring the epoch sees whole.  The
+// round-robin counter and the admission state stay device-owned.
+__global__ void route_update_kernel(Route* d, const Route nr, DestDesc* desc_slot, const DestDesc desc,
+                                    uint32_t new_dest) {
+  if (threadIdx.x != 0) return;
+  if (new_dest) *desc_slot = desc;
+  for (int i = 0; i < kMaxDests; ++i) d->dests[i] = nr.dests[i];
+  d->app_id = nr.app_id;
+  d->stage = nr.stage;
+  d->n = nr.n;
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&d->epoch), "r"(nr.epoch) : "memory");
+}
+cudaError_t launch_route_update(Route* d, const Route& nr, DestDesc* desc_slot, const DestDesc* desc, cudaStream_t s) {
+  route_update_kernel<<<1, 32, 0, s>>>(d, nr, desc_slot, desc ? *desc : DestDesc{}, desc ? 1u : 0u);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_engine_doorbell(EngineQueue* q, uint64_t b, const ring_msg_t* msgs, uint32_t* status, uint32_t n,
                                    uint32_t flags, bool wait, uint64_t timeout_ns, cudaStream_t s) {
   engine_doorbell_kernel<<<1, 32, 0, s>>>(q, b, msgs, status, n, flags, wait ? 1u : 0u, timeout_ns);
@@ -1382,6 +1403,7 @@ cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaSt
 cudaError_t preload_put() {
   cudaError_t e = preload_kernel(put_kernel<0>);
   if (e == cudaSuccess) e = preload_kernel(engine_doorbell_kernel);
+  if (e == cudaSuccess) e = preload_kernel(route_update_kernel);
   if (e == cudaSuccess) e = preload_kernel(engine_stop_kernel);
   if (e == cudaSuccess) e = preload_kernel(engine_wait_kernel);
   if (e == cudaSuccess) e = preload_kernel(put_kernel<1>, (int)cudaSharedmemCarveoutMaxShared);

@@ -279,6 +279,7 @@ cudaError_t launch_release(const ReleaseArgs& a, cudaStream_t s);
 cudaError_t launch_engine_doorbell(EngineQueue* q, uint64_t b, const ring_msg_t* msgs, uint32_t* status, uint32_t n,
                                    uint32_t flags, bool wait, uint64_t timeout_ns, cudaStream_t s);
 cudaError_t launch_engine_stop(EngineQueue* q, cudaStream_t s);
+cudaError_t launch_route_update(Route* d, const Route& nr, DestDesc* desc_slot, const DestDesc* desc, cudaStream_t s);
 cudaError_t launch_probe_ping(uint64_t* remote, const uint64_t* local, uint32_t iters, uint64_t* t_send,
                               uint64_t* rtt, uint64_t timeout_ns, cudaStream_t s);
 cudaError_t launch_probe_pong(uint64_t* remote, const uint64_t* local, uint32_t iters, uint64_t* t_seen,

@@ -372,7 +372,7 @@ def test_c5b_epoch_flip(R, cross):
                 R.ring_release(ring, 1, s)
         for p, P in enumerate(prod):
             R.ring_put_routed(P["rt"], P["msgs"][: half * 48], half, 0, P["st"][:half], P["dest"][:half], P["s"])
-        for p, P in enumerate(prod[:2]):      # reassignment (host-synchronises the producer's stream)
+        for p, P in enumerate(prod[:2]):      # reassignment: a device-side epoch flip in the producer's stream
             R.router_set_route(P["rt"], 7, 2, [P["pa"], P["pb"]], P["s"])    # epoch 2
             R.ring_put_routed(P["rt"], P["msgs"][half * 48:], M - half, 0, P["st"][half:], P["dest"][half:], P["s"])
         for d in set(devs):
