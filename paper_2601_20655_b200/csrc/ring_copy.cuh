@@ -149,6 +149,11 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
   bool have_first = true;
   // debug timeline: the first unit of the first copy warp of each CTA
   uint64_t* tr = (trace && (threadIdx.x >> 5) == (blockIdx.x == 0 ? 2 : 0)) ? trace + 1280 + 4 * blockIdx.x : nullptr;
+  // The item of the last unit, cached: consecutive units usually belong to the
+  // same entry, and its plan cannot change while this warp still holds one of
+  // its units (the slot is reused only after the item is published).
+  uint32_t c_item = 0xffffffffu, c_fu = 0, c_nu = 0;
+  uint64_t c_src = 0, c_dst = 0, c_len = 0;
   while (true) {
     uint32_t u = 0, quit = 0, ps = 0;
     if (lane == 0) {
@@ -171,9 +176,12 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
     if (quit) return;
     u = __shfl_sync(0xffffffffu, u, 0);
     ps = __shfl_sync(0xffffffffu, ps, 0);
-    uint32_t item = 0xffffffffu, fu = 0;
+    uint32_t item = 0xffffffffu, fu = 0, nu_hit = 0;
     uint64_t src = 0, dst = 0, len = 0;
-    if (spec && u < spec->n_units) {           // the CTA's own evaluation of the first rounds (shared memory)
+    if (c_nu && u - c_fu < c_nu) {             // same entry as the previous unit: no plan read
+      item = c_item; fu = c_fu; nu_hit = c_nu; src = c_src; dst = c_dst; len = c_len;
+    }
+    if (item == 0xffffffffu && spec && u < spec->n_units) {   // the CTA's own evaluation of the first rounds
       for (uint32_t b = 0; b < spec->n; b += 32) {
         const uint32_t i = b + lane;
         const bool in = i < spec->n;
@@ -184,6 +192,7 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
           const SpecItem& sh = spec->it[b + __ffs(m) - 1];
           item = sh.item;
           fu = sh.first_unit;
+          nu_hit = sh.nunits;
           src = sh.src;
           dst = sh.dst;
           len = sh.len;
@@ -211,11 +220,13 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
         dst = __shfl_sync(0xffffffffu, q0.y, h);
         len = __shfl_sync(0xffffffffu, q1.x, h);
         fu = (uint32_t)__shfl_sync(0xffffffffu, q1.y, h);
+        nu_hit = (uint32_t)(__shfl_sync(0xffffffffu, q1.y, h) >> 32);
         break;
       }
     }
     if (item == 0xffffffffu) return;   // cannot happen with a consistent plan
     cur = item;
+    c_item = item; c_fu = fu; c_nu = nu_hit; c_src = src; c_dst = dst; c_len = len;
     const uint32_t c = u - fu;
     const uint64_t lo = (uint64_t)c * chunk;
     const uint64_t hi = min(len, lo + chunk);
