@@ -74,6 +74,11 @@ __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8
   }
 }
 
+__device__ __forceinline__ uint32_t units_for(uint64_t len, uint32_t chunk) {
+  // an empty payload has no unit: entry headers are written by the put's publisher
+  return (uint32_t)((len + chunk - 1) >> (__ffs(chunk) - 1));
+}
+
 // Zero the counter set a launch will hand to its successor.
 __device__ __forceinline__ void reset_set(LaunchSet* s, int lane) {
   for (int i = lane; i < kPlanRing; i += 32) s->arrive[i] = 0;
@@ -349,22 +354,43 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
   uint32_t pending_u = 0xffffffffu;         // unit taken, not resolved yet
   bool exhausted = false;
   uint64_t wait_end = 0;
-  uint32_t n_taken = 0, first = 0;          // the first STAGES units come from one atomicAdd
-  if (lane == 0) first = atomicAdd(&S->next_unit, (uint32_t)STAGES);
-  first = __shfl_sync(0xffffffffu, first, 0);
+  // Control kept off the per-unit path (one warp drives all of a CTA's
+  // copies): units are taken kTake at a time (one atomicAdd), the `planned`
+  // word is re-read only when a unit is past the cached one, and the entry of
+  // the last unit is cached (consecutive units usually share it).
+  constexpr uint32_t kTake = 2 * STAGES;
+  uint32_t q_next = 0, q_end = 0;
+  uint64_t pl_cache = 0;
+  uint32_t c_item = 0xffffffffu, c_fu = 0, c_nu = 0;
+  uint64_t c_src = 0, c_dst = 0, c_len = 0;
+  if (lane == 0) {
+    q_next = atomicAdd(&S->next_unit, kTake);
+    q_end = q_next + kTake;
+  }
   while (true) {
     bool progress = false;
     // ---- 1. resolve the next unit and load it into a free stage
     if (!exhausted && k_issue - k_free < (uint32_t)STAGES) {
       uint32_t u = 0, state = 0, ps = 0;    // 0 = planned, 1 = not yet, 2 = none left
       if (lane == 0) {
-        if (pending_u == 0xffffffffu)
-          pending_u = n_taken < (uint32_t)STAGES ? first + n_taken : atomicAdd(&S->next_unit, 1u);
+        if (pending_u == 0xffffffffu) {
+          if (q_next == q_end) {
+            q_next = atomicAdd(&S->next_unit, kTake);
+            q_end = q_next + kTake;
+          }
+          pending_u = q_next++;
+        }
         u = pending_u;
         if (!(spec && u < spec->n_units)) {
-          const uint64_t pl = ld_acquire<false>(&S->planned);
-          if (planned_units(pl) <= u) state = planned_done(pl) ? 2 : 1;
-          else ps = planned_items(pl);
+          if (planned_units(pl_cache) <= u && !planned_done(pl_cache)) {
+            const uint64_t pl = ld_relaxed<false>(&S->planned);
+            if (pl != pl_cache) {
+              fence_acq_rel<false>();       // acquire the plans behind the new word
+              pl_cache = pl;
+            }
+          }
+          if (planned_units(pl_cache) <= u) state = planned_done(pl_cache) ? 2 : 1;
+          else ps = planned_items(pl_cache);
         }
       }
       state = __shfl_sync(0xffffffffu, state, 0);
@@ -382,18 +408,26 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
         u = __shfl_sync(0xffffffffu, u, 0);
         ps = __shfl_sync(0xffffffffu, ps, 0);
         pending_u = 0xffffffffu;
-        ++n_taken;
-        uint32_t item, fu = 0;
+        uint32_t item = 0xffffffffu, fu = 0;
         uint64_t src = 0, dst = 0, len = 0;
-        spec_lookup(spec, u, lane, item, fu, src, dst, len);
-        if (item == 0xffffffffu) {
-          item = find_item(ctx, u, cur, ps, lane);
+        if (c_nu && u - c_fu < c_nu) {      // same entry as the previous unit
+          item = c_item; fu = c_fu; src = c_src; dst = c_dst; len = c_len;
+        } else {
+          spec_lookup(spec, u, lane, item, fu, src, dst, len);
+          uint32_t nu = 0;
           if (item != 0xffffffffu) {
-            const Plan& p = ctx->plan[item % kPlanRing];
-            src = ld_cg64(&p.src); dst = ld_cg64(&p.dst); len = ld_cg64(&p.len);
-            fu = ld_cg32(&p.first_unit);
-            cur = item;
+            nu = units_for(len, chunk);
+          } else {
+            item = find_item(ctx, u, cur, ps, lane);
+            if (item != 0xffffffffu) {
+              const Plan& p = ctx->plan[item % kPlanRing];
+              src = ld_cg64(&p.src); dst = ld_cg64(&p.dst); len = ld_cg64(&p.len);
+              fu = ld_cg32(&p.first_unit);
+              nu = ld_cg32(&p.nunits);
+              cur = item;
+            }
           }
+          if (item != 0xffffffffu) { c_item = item; c_fu = fu; c_nu = nu; c_src = src; c_dst = dst; c_len = len; }
         }
         if (item == 0xffffffffu) {
           exhausted = true;
@@ -469,10 +503,6 @@ __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-__device__ __forceinline__ uint32_t units_for(uint64_t len, uint32_t chunk) {
-  // an empty payload has no unit: entry headers are written by the put's publisher
-  return (uint32_t)((len + chunk - 1) >> (__ffs(chunk) - 1));
-}
 
 // Load the CRC slicing tables into shared memory (whole CTA participates).
 __device__ __forceinline__ void load_crc_table(uint32_t* s_tab, const uint32_t* g_tab) {
