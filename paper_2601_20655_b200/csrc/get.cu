@@ -63,12 +63,15 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
         if (a.flags & RING_TRY) {
           st = RING_EMPTY;
         } else {
+          // relaxed polls, one acquire fence once the tail moved (an acquire
+          // per poll invalidates this SM's L1 under the copy warps' loads)
           const uint64_t end = globaltimer() + a.timeout_ns;
           do {
-            T = ld_acquire<SYS>(g_tail(a.ring));
+            T = ld_relaxed<SYS>(g_tail(a.ring));
             if (globaltimer() > end) break;
           } while (ptr_seq(T) == ptr_seq(G));
           if (ptr_seq(T) == ptr_seq(G)) st = RING_ETIMEDOUT;
+          else fence_acq_rel<SYS>();
         }
       }
       tvis = (a.flags & RING_NO_TIMESTAMP) ? 0 : globaltimer();

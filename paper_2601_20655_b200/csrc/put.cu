@@ -41,6 +41,12 @@ __device__ __forceinline__ uint64_t read_head(const DestDesc& d) {
   return d.sys ? ld_acquire<true>(head_w(d)) : ld_acquire<false>(head_w(d));
 }
 
+__device__ __forceinline__ uint64_t read_head_relaxed(const DestDesc& d) {
+  const uint64_t m = d.sys ? ld_relaxed<true>(&d.st->mirror_head) : ld_relaxed<false>(&d.st->mirror_head);
+  if (m & kMirrorValid) return m & ~kMirrorValid;
+  return d.sys ? ld_relaxed<true>(head_w(d)) : ld_relaxed<false>(head_w(d));
+}
+
 __device__ __forceinline__ void st_u32_relaxed_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -342,11 +348,14 @@ __device__ uint32_t leader_place(const PutArgs& a, uint32_t flags, LaunchCtx* ct
         st_release<false>(&S->planned, make_planned(L.items, L.units));
         if (!t_start) t_start = globaltimer();
         if (a.trace) { a.trace[1906] = globaltimer(); a.trace[1907] = P; a.trace[1908] = H2; a.trace[1909] = f; a.trace[1910]++; }
+        // relaxed polls (an acquire per poll invalidates the SM's L1, where the
+        // copy warps' loads are staged), one acquire fence once the head moved
         uint64_t H3 = H2;
         while (H3 == H2) {
           if (globaltimer() - t_start > a.timeout_ns) break;
-          H3 = read_head(D);
+          H3 = read_head_relaxed(D);
         }
+        if (H3 != H2) { if (D.sys) fence_acq_rel<true>(); else fence_acq_rel<false>(); }
         if (H3 == H2) { o.status = RING_ETIMEDOUT; break; }
         L.heads[d] = H3;
       }
