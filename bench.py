@@ -758,6 +758,11 @@ def bench_pairs(args, rank, world, grp):
                    "l2": "inputs larger than L2 per rank (2 x 128 MiB source sets)",
                    "parallelism": f"{world} concurrent SPSC rings (one egress + one ingress stream per GPU)"},
         "per_gpu_gbs": round(per_gpu, 2),
+        # forward bytes on the link per message = footprint +
+        # size slot + tail word (the ncu counters add the link protocol on top:
+        # profiles/r02_ncu_nvlink_counters.csv, 1.21 wire bytes per payload byte)
+        "wire_gbs_per_gpu_algorithmic": round(per_gpu * sum(R.ring_footprint(C3_LENS[q % 2]) + 16 for q in range(m))
+                                              / payload_step, 2),
         "nvlink_frac_of_900": round(per_gpu / NVLINK_NOMINAL, 4),
         "nvlink_ce": ce,
         "nvlink_frac_of_ce": round(per_gpu / ce["bidir_per_direction_gbs"], 4) if ce else None,
