@@ -979,13 +979,16 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
 // `stream` comes after the queue reset, never after the engine.
 static ring_status_t engine_launch(ring_peer_t p, void* stream) {
   DevGuard g(p->device);
-  if (!p->eq) {
-    CUDA_TRY(cudaMalloc(&p->eq, sizeof(EngineQueue)));
+  // each resource on its own: a failed first start leaves nothing half-made behind
+  if (!p->eq) CUDA_TRY(cudaMalloc(&p->eq, sizeof(EngineQueue)));
+  if (!p->eh) {
     CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&p->eh), sizeof(EngineHost), cudaHostAllocMapped));
-    CUDA_TRY(cudaStreamCreateWithFlags(&p->eng_stream, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&p->eng_exit, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&p->eng_ready, cudaEventDisableTiming));
+    p->eh->lease = 0;
+    p->eh->alive = 0;
   }
+  if (!p->eng_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->eng_stream, cudaStreamNonBlocking));
+  if (!p->eng_exit) CUDA_TRY(cudaEventCreateWithFlags(&p->eng_exit, cudaEventDisableTiming));
+  if (!p->eng_ready) CUDA_TRY(cudaEventCreateWithFlags(&p->eng_ready, cudaEventDisableTiming));
   p->eh->lease = p->eh->lease + 1;
   p->eh->alive = 1u;
   CUDA_TRY(cudaEventRecord(p->eng_ready, as_stream(stream)));
