@@ -398,6 +398,11 @@ ring_status_t ring_read_data(ring_t ring, uint64_t offset, uint64_t len, void* h
  * %globaltimer timeline of its leader rounds and publisher runs; copy the last
  * one (up to n words) to host memory.  RING_EINVAL if tracing is off. */
 ring_status_t ring_peer_trace(ring_peer_t peer, uint64_t* host_out, uint32_t n);
+/* Debug timeline of the copy-out gets of a ring (B200RING_TRACE=1 at the first
+ * get): words [0,510) = (%globaltimer, items planned) per control round,
+ * [512,1022) = (%globaltimer, entries released) per finisher release, both
+ * rings of 255 pairs; n <= 1024 words. */
+ring_status_t ring_get_trace(ring_t ring, uint64_t* host_out, uint32_t n);
 ring_status_t ring_write_data(ring_t ring, uint64_t offset, uint64_t len, const void* host_src);
 
 /* ---- stage router (PAPER.md:524-532 round-robin ResultDeliver; PAPER.md:914-924

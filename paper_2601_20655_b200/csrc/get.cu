@@ -190,7 +190,14 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
       items += e2;
       units += __shfl_sync(0xffffffffu, nu_incl, 31);
       __syncwarp();
-      if (lane == 0) st_release<false>(&S->planned, make_planned(items, units));
+      if (lane == 0) {
+        st_release<false>(&S->planned, make_planned(items, units));
+        if (a.trace) {
+          const uint32_t k = atomicAdd(reinterpret_cast<unsigned int*>(a.trace + 1023), 1u) % 255;
+          a.trace[2 * k] = globaltimer();
+          a.trace[2 * k + 1] = items;
+        }
+      }
     }
     // ---- steps 4-5 (no copy-out): clear busy bits, move the head past the batch
     const uint32_t first_msg = msgmask ? (uint32_t)__ffs(msgmask) - 1 : 32u;
@@ -284,7 +291,14 @@ __device__ void get_finisher(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S) {
       uint64_t hb = ptr_off(H) + fsum;
       if (hb >= a.R) hb -= a.R;
       H = pack_ptr(hb, ptr_seq(H) + nrel);
-      if (lane == 0) publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
+      if (lane == 0) {
+        publish_head<SYS>(a.ring, a.mirrors, a.n_mirrors, H);
+        if (a.trace) {
+          const uint32_t k = atomicAdd(reinterpret_cast<unsigned int*>(a.trace + 1022), 1u) % 255;
+          a.trace[512 + 2 * k] = globaltimer();
+          a.trace[512 + 2 * k + 1] = i + run;
+        }
+      }
     }
     i += run;
     if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&S->pub_seq), "r"(i) : "memory");

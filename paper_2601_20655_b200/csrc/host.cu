@@ -193,6 +193,7 @@ struct ring_s {
   uint8_t* data = nullptr;                   // buffer region (base + data_off, or the split allocation)
   uint8_t* hdrs = nullptr;                   // split placement: header copies in the control allocation
   int data_device = -1;                      // split placement: the GPU holding the buffer region
+  uint64_t* trace = nullptr;                 // debug timeline of the get kernels (B200RING_TRACE=1)
 };
 
 struct ring_peer_s {
@@ -479,6 +480,7 @@ ring_status_t ring_destroy(ring_t r) {
   for (void* p : r->opened) cudaIpcCloseMemHandle(p);
   cudaFree(r->ctx);
   cudaFree(r->mirrors_dev);
+  if (r->trace) cudaFree(r->trace);
   if (r->owner) cudaFree(r->base);
   else if (r->ipc_opened) cudaIpcCloseMemHandle(r->base);
   if (r->owner && r->data_device >= 0) {
@@ -862,6 +864,14 @@ ring_status_t ring_peer_set_fault(ring_peer_t p, const ring_fault_t* f) {
   return RING_OK;
 }
 
+ring_status_t ring_get_trace(ring_t r, uint64_t* host_out, uint32_t n) {
+  if (!r || !host_out || !r->trace || n > 1024) return RING_EINVAL;
+  DevGuard g(r->device);
+  CUDA_TRY(quiesce());
+  CUDA_TRY(cudaMemcpy(host_out, r->trace, 8ull * n, cudaMemcpyDeviceToHost));
+  return RING_OK;
+}
+
 ring_status_t ring_peer_trace(ring_peer_t p, uint64_t* host_out, uint32_t n) {
   if (!p || !host_out) return RING_EINVAL;
   if (!p->trace) return RING_EINVAL;
@@ -1117,6 +1127,13 @@ static ring_status_t get_common(ring_t r, uint32_t n, ring_view_t* d_views, void
   a.ring = r->base;
   a.data = r->data;
   a.hdrs = r->hdrs;
+  if (getenv("B200RING_TRACE")) {
+    if (!r->trace) {
+      CUDA_TRY(cudaMalloc(&r->trace, 1024 * 8));
+      CUDA_TRY(cudaMemset(r->trace, 0, 1024 * 8));
+    }
+    a.trace = r->trace;
+  }
   a.views = d_views;
   a.dst = static_cast<uint8_t*>(d_dst);
   a.mirrors = r->mirrors_dev;

@@ -260,6 +260,7 @@ struct GetArgs {
   uint32_t sys;         // producers may be remote: .sys scope
   uint32_t n_mirrors;
   uint32_t chunk;
+  uint64_t* trace;      // debug timeline (B200RING_TRACE=1): [0,512) control rounds, [512,1024) releases
 };
 
 struct ReleaseArgs {

@@ -108,6 +108,7 @@ def _load():
         "ring_clock_offset_ns": [I, C.POINTER(C.c_int64)],
         "ring_probe_rtt": [I, I, U32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int64)],
         "ring_peer_trace": [P, P, U32],
+        "ring_get_trace": [P, P, U32],
         "ring_peer_set_fault": [P, C.POINTER(ring_fault_t)],
         "ring_set_lock_timeout_ns": [U64],
         "ring_set_hole_timeout_ns": [U64],
@@ -258,6 +259,12 @@ def ring_peer_engine_state(peer: int) -> dict:
 
 def ring_peer_submitted(peer: int) -> int:
     return int(lib.ring_peer_submitted(peer))
+
+
+def ring_get_trace(ring: int, n: int = 1024) -> np.ndarray:
+    out = np.zeros(n, dtype=np.uint64)
+    _check("ring_get_trace", lib.ring_get_trace(ring, out.ctypes.data, n))
+    return out
 
 
 def ring_peer_trace(peer: int, n: int = 4096) -> np.ndarray:
