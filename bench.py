@@ -543,8 +543,11 @@ def bench_pairs(args, rank, world, grp):
     from paper_2601_20655_b200 import topology as T
     dev = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(dev)
-    Rb, N = 64 << 20, 64
-    m = args.msgs_per_step or 32
+    # 256 MiB rings, 128 messages (512 MiB) per put / consume launch: per-launch
+    # start and drain amortised over ~0.8 ms (64 MiB / 32 per launch: -9 %,
+    # profiles/r02_c3_sweep.txt)
+    Rb, N = (args.ring_mb or 256) << 20, 64
+    m = args.msgs_per_step or 128
     pull = bool(args.pull)
     own = None
     if args.pull == 2:
@@ -755,7 +758,7 @@ def bench_pairs(args, rank, world, grp):
                    "placement": {0: "push (ring at the consumer)", 1: "pull (ring_open)",
                                  2: "split (ring_create_split)"}[args.pull],
                    "R_bytes": Rb, "n_slots": N, "msgs_per_step_per_rank": m,
-                   "l2": "inputs larger than L2 per rank (2 x 128 MiB source sets)",
+                   "l2": f"inputs larger than L2 per rank (2 x {m * 4} MiB source sets)",
                    "parallelism": f"{world} concurrent SPSC rings (one egress + one ingress stream per GPU)"},
         "per_gpu_gbs": round(per_gpu, 2),
         # forward bytes on the link per message = footprint +
@@ -797,45 +800,155 @@ def bench_pairs(args, rank, world, grp):
     }
 
 
-def measure_ce(a: int, b: int, nbytes: int = 256 << 20, reps: int = 10) -> dict:
-    """In-run copy-engine NVLink peak (cudaMemcpyPeerAsync via torch copies):
-    GPU a -> GPU b alone, and a -> b with b -> a at the same time."""
+def bench_c3_one_way(args, rank, world, grp, placement: str):
+    """BASELINE.json configs[2] as the north star states its target: ONE ring,
+    GPU 0 -> GPU 1, 4-MB Wan2.1 tensors, GB/s per direction against 900.
+    placement "split" (ring_create_split, R28: control words and header copies
+    at the consumer, buffer region at the producer; the copy-out consume pulls
+    every payload over NVLink) or "push" (the paper's one-sided write into the
+    consumer's ring).  256 MiB ring, 64 messages per put / consume launch.
+    Payloads come from the seeded device generator; the last timed launch's
+    copy-out (split) or ring entries (push) are compared with it on the device.
+    Ranks >= 2 only take part in the collectives.  Returns the result on rank 0."""
     import torch
-    x = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{a}")
-    y = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{b}")
-    x2 = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{b}")
-    y2 = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{a}")
+    import torch.distributed as dist
+    from paper_2601_20655_b200 import ring as R
+    from synth import device as SD
+    dev = int(os.environ.get("LOCAL_RANK", rank))
+    Rb, N, K, launches, warm = 256 << 20, 64, 64, int(os.environ.get("B200RING_C3_LAUNCHES", 40)), 2
+    stride, seed = 4194304, synth_seed_c3()
+    lens = [C3_LENS[q % 2] for q in range(K)]
+    split = placement == "split"
+    ring = peer = None
+    hs = [None] * world
+    if rank == 1:
+        ring = (R.ring_create_split(dev, (dev - 1) % torch.cuda.device_count(), Rb, N, 1, 0) if split
+                else R.ring_create(dev, Rb, N, 1, 0))
+        hs[1] = R.ring_export(ring)
+    dist.all_gather_object(hs, hs[1] if rank == 1 else None, group=grp)
+    mh = None
+    if rank == 0:
+        peer, mh = R.ring_attach_peer(hs[1], dev, 0)
+    mhs = [None] * world
+    dist.all_gather_object(mhs, mh, group=grp)
+    if rank == 1:
+        R.ring_bind_mirror(ring, 0, mhs[0])
+    res = torch.zeros(4, dtype=torch.float64)
+    if rank in (0, 1):
+        s = torch.cuda.Stream()
+        if rank == 0:
+            src = torch.empty(K * stride, dtype=torch.uint8, device="cuda")
+            keep = SD.fill([src.data_ptr() + q * stride for q in range(K)], lens, [0] * K, list(range(K)), seed)
+            a = R.make_msgs([src.data_ptr() + q * stride for q in range(K)], lens, [bytes(16)] * K, [0] * K,
+                            list(range(K)), [2] * K)
+            d_msgs = torch.from_numpy(a.view(np.uint8).copy()).cuda()
+            status = torch.zeros(K, dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()
+            del keep
+            run = lambda: R.ring_put_batch(peer, d_msgs, K, 0, status, s)
+        else:
+            views = torch.zeros(K * 128, dtype=torch.uint8, device="cuda")
+            dst = torch.empty(K * stride, dtype=torch.uint8, device="cuda") if split else None
+            run = lambda: R.ring_consume(ring, K, views, dst, stride if split else 0, 0, s)
+        for _ in range(warm):
+            run()
+        torch.cuda.synchronize()
+        dist.barrier(group=grp)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(launches):
+            run()
+        e1.record(s)
+        torch.cuda.synchronize()
+        res[0] = e0.elapsed_time(e1)
+        if rank == 0:
+            res[1] = float(bool((status == 0).all().item()))
+        else:
+            v = R.parse_views(views.cpu().numpy())
+            res[1] = float(bool((v["status"] == 0).all()))
+            if split:
+                bad = SD.verify([dst.data_ptr() + q * stride for q in range(K)], lens, [0] * K, list(range(K)), seed)
+            else:
+                # push: the last launch's entries are still in the ring (released, not overwritten)
+                base = R.ring_get_info(ring).data
+                bad = SD.verify([base + int(o) for o in v["offset"]], lens, [0] * K, list(range(K)), seed)
+            torch.cuda.synchronize()
+            res[2] = float(int((bad.cpu() != -1).sum()))
+        res[3] = 1.0
+    dist.barrier(group=grp)
+    out = [None] * world
+    dist.all_gather_object(out, res.tolist(), group=grp)
+    if rank == 0:
+        R.ring_detach(peer)
+    dist.barrier(group=grp)
+    if rank == 1:
+        R.ring_destroy(ring)
+    if rank != 0:
+        return None
+    ms = max(out[0][0], out[1][0])
+    gbs = sum(lens) * launches / (ms / 1e3) / 1e9
+    return {"placement": placement, "value": round(gbs, 1), "unit": "GB/s (payload, one direction)",
+            "nvlink_frac_of_900": round(gbs / NVLINK_NOMINAL, 4), "ms": round(ms, 3),
+            "ms_producer": round(out[0][0], 3), "ms_consumer": round(out[1][0], 3),
+            "ok": out[0][1] == 1.0 and out[1][1] == 1.0 and out[1][2] == 0.0,
+            "verified": {"payload_mismatches": int(out[1][2]), "messages": K,
+                         "what": "the last timed launch's payloads compared on the consumer GPU with the seeded "
+                                 "generator (synth/csrc/synth_dev.cu)"},
+            "config": {"workload": "C3 (BASELINE.json configs[2]) one ring GPU 0 -> GPU 1, Wan2.1 umT5 emb / 480p "
+                                   "latent alternating (4,194,304 / 4,193,280 B)",
+                       "R_bytes": Rb, "n_slots": N, "msgs_per_launch": K, "launches_timed": launches,
+                       "timing": "CUDA events on the producer's and the consumer's stream, max of the two"}}
+
+
+def synth_seed_c3():
+    import synth
+    return synth.SEED_BASE + 33
+
+
+def measure_ce(a: int, b: int, nbytes: int = 256 << 20, reps: int = 10) -> dict:
+    """In-run copy-engine NVLink reference: cudaMemcpyPeerAsync (cuda-python),
+    GPU a -> GPU b alone, then a -> b and b -> a at the same time, each
+    direction issued on a stream of its source GPU and timed by its own CUDA
+    events (per direction: the slower of the two)."""
+    import torch
+    from cuda.bindings import runtime as rt
+    for x, y in ((a, b), (b, a)):
+        with torch.cuda.device(x):
+            rt.cudaDeviceEnablePeerAccess(y, 0)     # "already enabled" is fine
+    xa = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{a}")
+    yb = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{b}")
+    xb = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{b}")
+    ya = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{a}")
     sa, sb = torch.cuda.Stream(a), torch.cuda.Stream(b)
-    for _ in range(2):
-        with torch.cuda.stream(sa):
-            y.copy_(x, non_blocking=True)
-    torch.cuda.synchronize(a)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(sa):
-        e0.record(sa)
+
+    def copies(dst, dd, src, sd, st):
         for _ in range(reps):
-            y.copy_(x, non_blocking=True)
-        e1.record(sa)
-    torch.cuda.synchronize(a)
-    one = nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
-    # both directions at once: the bytes of both over the union of their
-    # windows (host clock around the pair; ~2 x 2.7 GB, launch cost negligible)
-    torch.cuda.synchronize(a)
-    torch.cuda.synchronize(b)
-    t0 = time.perf_counter()
-    with torch.cuda.stream(sa):
-        for _ in range(reps):
-            y.copy_(x, non_blocking=True)
-    with torch.cuda.device(b), torch.cuda.stream(sb):
-        for _ in range(reps):
-            y2.copy_(x2, non_blocking=True)
-    torch.cuda.synchronize(a)
-    torch.cuda.synchronize(b)
-    bi = nbytes * reps / (time.perf_counter() - t0) / 1e9
-    del x, y, x2, y2
-    return {"one_direction_gbs": round(one, 1), "bidir_per_direction_gbs": round(bi, 1),
-            "what": f"cudaMemcpyPeerAsync {nbytes >> 20} MiB x {reps}, GPU {a} -> {b} alone (events) and with {b} -> {a} "
-                    "concurrently (per direction: bytes of one direction over the host-timed union window)"}
+            err, = rt.cudaMemcpyPeerAsync(dst.data_ptr(), dd, src.data_ptr(), sd, nbytes, st.cuda_stream)
+            assert err == rt.cudaError_t.cudaSuccess, err
+
+    def timed(jobs):
+        for d in (a, b):
+            torch.cuda.synchronize(d)
+        ev = []
+        for dst, dd, src, sd, st in jobs:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.device(sd):
+                e0.record(st)
+                copies(dst, dd, src, sd, st)
+                e1.record(st)
+            ev.append((e0, e1))
+        for d in (a, b):
+            torch.cuda.synchronize(d)
+        return [nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9 for e0, e1 in ev]
+
+    timed([(yb, b, xa, a, sa)])                                   # warm
+    one = timed([(yb, b, xa, a, sa)])[0]
+    bi = timed([(yb, b, xa, a, sa), (ya, a, xb, b, sb)])
+    del xa, yb, xb, ya
+    return {"one_direction_gbs": round(one, 1), "bidir_per_direction_gbs": round(min(bi), 1),
+            "bidir_gbs": [round(x, 1) for x in bi],
+            "what": f"cudaMemcpyPeerAsync {nbytes >> 20} MiB x {reps}, GPU {a} -> {b} alone and with {b} -> {a} "
+                    "concurrently (each direction on a stream of its source GPU, its own CUDA events)"}
 
 
 def R_clock_offset(dev):
@@ -896,6 +1009,7 @@ def main():
     ap.add_argument("--lat-iters", type=int, default=560,
                     help="N>1: unloaded-latency round trips per size per rank (>= 1,000 samples pooled at N=2)")
     ap.add_argument("--no-overlap", action="store_true", help="N=1: put(s+1) waits for consume(s)")
+    ap.add_argument("--ring-mb", type=int, default=0, help="N>1 pairs: ring data region in MiB (0 = 256)")
     ap.add_argument("--cons-ctas", type=int, default=0, help="N>1 pull: consumer copy-out grid (0 = default)")
     ap.add_argument("--cons-threads", type=int, default=0)
     ap.add_argument("--pull", type=int, default=0,
@@ -953,6 +1067,7 @@ def main():
             extra = {}
             offsets = [None] * world
             dist.all_gather_object(offsets, R_clock_offset(local), group=grp)
+            extra["c3_one_way"] = {pl: bench_c3_one_way(args, rank, world, grp, pl) for pl in ("split", "push")}
             if world >= 4:
                 a4 = copy.copy(args)
                 a4.steps, a4.warmup, a4.msgs_per_step = 10, 3, 2
@@ -968,6 +1083,9 @@ def main():
                 for k, v in extra.items():
                     if v is not None:
                         out[k] = v
+                if out.get("c3_one_way"):
+                    best = max(out["c3_one_way"].values(), key=lambda r: r["value"] if r["ok"] else 0)
+                    out["c3_one_way"]["best"] = best["placement"]
         if out:
             print(json.dumps(out), flush=True)
     finally:

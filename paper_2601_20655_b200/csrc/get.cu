@@ -167,7 +167,9 @@ __device__ void get_control(const GetArgs& a, LaunchCtx* ctx, LaunchSet* S, cons
       // Plan slots still in use by the copy warps / finisher are never
       // overwritten: on a flow-control timeout the batch is left unread.
       if (__shfl_sync(0xffffffffu, flow_to, 0)) { fail = RING_ETIMEDOUT; break; }
-      uint32_t nu = (in && deliver) ? units_for(len, a.chunk) : 0;
+      // remote buffer region: units on the payload's 128-B lines (copy_warp align_src)
+      const uint32_t sh = a.remote_data ? (uint32_t)(reinterpret_cast<uintptr_t>(a.data + start + kHdr) & 127u) : 0u;
+      uint32_t nu = (in && deliver && len) ? units_for(len + sh, a.chunk) : 0;
       uint32_t nu_incl = nu;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -310,7 +312,7 @@ __device__ void release_held(uint8_t* ring, uint64_t** mirrors, uint32_t n_mirro
                              uint32_t count);
 
 template <bool SYS>
-__global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
+__global__ void __maxnreg__(120) get_kernel(const GetArgs a) {
   LaunchCtx* ctx = a.ctx;
   LaunchSet* S = &ctx->set[a.launch & 1];
   const int warp = threadIdx.x >> 5;
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(512, 1) get_kernel(const GetArgs a) {
     }
   }
   if (blockIdx.x != 0) __syncthreads();
-  if (a.dst) copy_warp<3>(ctx, S, &cs, a.chunk, a.timeout_ns);
+  if (a.dst) copy_warp<3>(ctx, S, &cs, a.chunk, a.timeout_ns, nullptr, nullptr, a.remote_data != 0);
 }
 
 // In-order release of `count` received entries plus the PAD entries the read

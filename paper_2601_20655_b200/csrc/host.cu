@@ -193,6 +193,7 @@ struct ring_s {
   uint8_t* data = nullptr;                   // buffer region (base + data_off, or the split allocation)
   uint8_t* hdrs = nullptr;                   // split placement: header copies in the control allocation
   int data_device = -1;                      // split placement: the GPU holding the buffer region
+  bool remote_data = false;                  // split / pull placement: the buffer region is on another GPU
   uint64_t* trace = nullptr;                 // debug timeline of the get kernels (B200RING_TRACE=1)
 };
 
@@ -439,6 +440,7 @@ ring_status_t ring_create_split(int device, int data_device, uint64_t data_bytes
   ring_s* r = new ring_s;
   r->device = device;
   r->data_device = data_device;
+  r->remote_data = data_device != device;
   r->R = data_bytes;
   r->N = n_slots;
   r->max_producers = max_producers;
@@ -515,6 +517,7 @@ ring_status_t ring_open(const ring_handle_t* h, int device, ring_t* out) {
   r->flags = b.flags;
   r->sys = 1;
   r->owner = false;
+  r->remote_data = b.device != device;
   if (b.data_ptr) { delete r; return RING_EINVAL; }   // split rings are consumed where their control words live
   r->data_off = data_offset(b.N);
   r->alloc = r->data_off + b.R;
@@ -1148,6 +1151,7 @@ static ring_status_t get_common(ring_t r, uint32_t n, ring_view_t* d_views, void
   a.consume = consume;
   a.sys = r->sys;
   a.n_mirrors = r->max_producers;
+  a.remote_data = r->remote_data;
   DevGuard g(r->device);
   uint32_t ctas = r->copy_ctas, thr = r->threads, chunk = r->chunk;
   default_grid(r->device, false, &ctas, &thr, &chunk);

@@ -1256,7 +1256,7 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
 // copy warps with 32-B accesses (NVLink destinations).  Separate kernels, so
 // one path's registers never change another's copy loop.
 template <int MODE>
-__global__ void __launch_bounds__(512, 1) put_kernel(const __grid_constant__ PutArgs a) {
+__global__ void __maxnreg__(96) put_kernel(const __grid_constant__ PutArgs a) {
   LaunchCtx* ctx = a.ctx;
   LaunchSet* S = &ctx->set[a.launch & 1];
   const int warp = threadIdx.x >> 5;

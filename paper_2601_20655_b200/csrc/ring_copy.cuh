@@ -8,7 +8,7 @@
 // the next unit with one atomicAdd (dynamic, warp-granular scheduling: small
 // and large entries mix without idle CTAs), waits until the control warp has
 // published a plan covering that unit, copies it through 16-byte integer
-// vector registers (R17: bit-exact, NaN payloads preserved; 8 loads in flight
+// vector registers (R17: bit-exact, NaN payloads preserved; 16 loads in flight
 // per lane), and arrives on arrive[item] with a gpu-scope release.  The
 // publisher / finisher warp that observes the full count then performs one
 // system-scope release (the tail store, or the head store for a consumer):
@@ -33,12 +33,59 @@ __device__ __forceinline__ uint64_t ld_cg64(const uint64_t* p) { return __ldcg(r
 #ifndef B200RING_COPY_U
 #define B200RING_COPY_U 16
 #endif
+#ifndef B200RING_TAIL_U
+#define B200RING_TAIL_U 4
+#endif
 template <int V = 1>
-__device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8_t* dst, uint64_t nb, int lane) {
+__device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8_t* dst, uint64_t nb, int lane,
+                                          bool align_src = false) {
+  // Copy-out loads on 128-B lines.  A payload starts 64 B into its 128-B
+  // aligned entry (kHdr), so a warp's 512-B load would touch five lines, four
+  // of them partially; pulled over NVLink (placements ring_open /
+  // ring_create_split) that costs ~1/7 of the link (profiles/r02_pull_align.txt).
+  // The loop starts at the line boundary below `src` instead: the lanes before
+  // `src` load bytes of the same line (the header or the previous unit, never
+  // outside the ring's data region) and store nothing; the stores then sit off
+  // their lines locally, which L2 takes at 32-B sector granularity.  Peeling
+  // the first bytes instead would cost each unit one dependent round trip.
+  // With align_src the units after an entry's first also start on lines
+  // (copy_warp), so only the first unit of each entry takes this path.  Local
+  // copy-out (the ring in this GPU's HBM) keeps its stores aligned instead
+  // (~1 % faster in C2, same-box A/B).
+  if (V == 3 && align_src && (((uintptr_t)src | (uintptr_t)dst) & 15) == 0 && ((uintptr_t)src & 127) &&
+      nb >= 1024) {
+    const uint32_t off16 = (uint32_t)(((uintptr_t)src & 127) >> 4);
+    const int4* s = reinterpret_cast<const int4*>(src) - off16;
+    int4* d = reinterpret_cast<int4*>(dst) - off16;
+    const uint32_t n16 = (uint32_t)(nb >> 4) + off16;
+    constexpr int U = B200RING_COPY_U;
+    uint32_t i = lane;
+    for (; i + (U - 1) * 32 < n16; i += U * 32) {
+      int4 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = ld_cg16(s + i + j * 32);
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (i + j * 32 >= off16) st16(d + i + j * 32, v[j]);
+    }
+    constexpr int T = B200RING_TAIL_U;   // the ragged rest: T loads in flight per lane, not one round trip per 512 B
+    for (; i < n16; i += T * 32) {
+      int4 v[T];
+#pragma unroll
+      for (int j = 0; j < T; ++j)
+        if (i + j * 32 < n16) v[j] = ld_cg16(s + i + j * 32);
+#pragma unroll
+      for (int j = 0; j < T; ++j)
+        if (i + j * 32 < n16 && i + j * 32 >= off16) st16(d + i + j * 32, v[j]);
+    }
+    const uint64_t done = (uint64_t)(n16 - off16) << 4;
+    for (uint64_t j = done + lane; j < nb; j += 32) dst[j] = __ldcg(src + j);
+    return;
+  }
   if (V == 2 && (((uintptr_t)src | (uintptr_t)dst) & 31) == 0) {
     const uint32_t n32 = (uint32_t)(nb >> 5);
-    uint32_t i = lane;
     constexpr int U = B200RING_COPY_U / 2;   // same 8 KiB in flight per warp
+    uint32_t i = lane;
     for (; i + (U - 1) * 32 < n32; i += U * 32) {
       v8u32 v[U];
 #pragma unroll
@@ -52,8 +99,8 @@ __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8
     const int4* s = reinterpret_cast<const int4*>(src);
     int4* d = reinterpret_cast<int4*>(dst);
     const uint32_t n16 = (uint32_t)(nb >> 4);
-    uint32_t i = lane;
     constexpr int U = B200RING_COPY_U;   // 16: 8 KiB in flight per warp
+    uint32_t i = lane;
     for (; i + (U - 1) * 32 < n16; i += U * 32) {
       int4 v[U];
 #pragma unroll
@@ -61,7 +108,16 @@ __device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8
 #pragma unroll
       for (int j = 0; j < U; ++j) st16(d + i + j * 32, v[j]);
     }
-    for (; i < n16; i += 32) st16(d + i, V == 3 ? ld_cg16(s + i) : ld_stream16(s + i));
+    constexpr int T = B200RING_TAIL_U;
+    for (; i < n16; i += T * 32) {
+      int4 v[T];
+#pragma unroll
+      for (int j = 0; j < T; ++j)
+        if (i + j * 32 < n16) v[j] = V == 3 ? ld_cg16(s + i + j * 32) : ld_stream16(s + i + j * 32);
+#pragma unroll
+      for (int j = 0; j < T; ++j)
+        if (i + j * 32 < n16) st16(d + i + j * 32, v[j]);
+    }
     for (uint64_t j = ((uint64_t)n16 << 4) + lane; j < nb; j += 32) dst[j] = V == 3 ? __ldcg(src + j) : src[j];
   } else if ((((uintptr_t)src | (uintptr_t)dst) & 3) == 0) {
     const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
@@ -142,7 +198,7 @@ __device__ __forceinline__ uint64_t wait_planned(LaunchSet* S, CopyShared* cs, u
 template <int V = 1>
 __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShared* cs, uint32_t chunk,
                                           uint64_t timeout_ns, uint64_t* trace = nullptr,
-                                          const SpecRound* spec = nullptr) {
+                                          const SpecRound* spec = nullptr, bool align_src = false) {
   const int lane = threadIdx.x & 31;
   uint32_t cur = 0;   // items before `cur` hold no unit this warp can still take
   // First unit: the CTA took a block of units for all its copy warps with ONE
@@ -233,11 +289,16 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
     cur = item;
     c_item = item; c_fu = fu; c_nu = nu_hit; c_src = src; c_dst = dst; c_len = len;
     const uint32_t c = u - fu;
-    const uint64_t lo = (uint64_t)c * chunk;
-    const uint64_t hi = min(len, lo + chunk);
+    // align_src: units after the first start on the source's 128-B lines (the
+    // first is `sh` bytes short; the control warp planned units_for(len + sh))
+    const uint32_t sh = align_src ? (uint32_t)(src & 127u) : 0u;
+    const uint64_t lo = c ? (uint64_t)c * chunk - sh : 0;
+    const uint64_t hi = min(len, (uint64_t)(c + 1) * chunk - sh);
     if (tr && lane == 0) tr[2] = globaltimer();
-    RING_CHECK(c < (uint32_t)((len + chunk - 1) / chunk) || len == 0, "unit inside its item", u, item);
-    if (hi > lo) warp_copy<V>(reinterpret_cast<const uint8_t*>(src) + lo, reinterpret_cast<uint8_t*>(dst) + lo, hi - lo, lane);
+    RING_CHECK(c < (uint32_t)((len + sh + chunk - 1) / chunk) || len == 0, "unit inside its item", u, item);
+    if (hi > lo)
+      warp_copy<V>(reinterpret_cast<const uint8_t*>(src) + lo, reinterpret_cast<uint8_t*>(dst) + lo, hi - lo, lane,
+                   align_src);
     __syncwarp();
     if (lane == 0) red_release_gpu_add(&S->arrive[item % kPlanRing], 1u);
     if (tr && lane == 0) tr[3] = globaltimer();

@@ -258,6 +258,7 @@ struct GetArgs {
   uint32_t flags;
   uint32_t consume;     // 1: release each entry after reading (and copying)
   uint32_t sys;         // producers may be remote: .sys scope
+  uint32_t remote_data;  // the buffer region is on another GPU (pull / split): copy-out loads on 128-B lines
   uint32_t n_mirrors;
   uint32_t chunk;
   uint64_t* trace;      // debug timeline (B200RING_TRACE=1): [0,512) control rounds, [512,1024) releases

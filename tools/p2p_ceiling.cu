@@ -3,7 +3,7 @@
 // once) with (1) the copy engine (cudaMemcpyPeerAsync), (2) a plain SM copy
 // kernel -- local loads, peer stores -- with 16-B and 32-B vectors over a grid
 // sweep, (3) SM peer stores of register data (no loads), (4) SM pull (peer loads,
-// local stores).  Build + run: nvcc -O3 -gencode arch=compute_100a,code=sm_100a
+// local stores), (5)-(7) both directions at once (push, pull, copy engines).  Build + run: nvcc -O3 -gencode arch=compute_100a,code=sm_100a
 // tools/p2p_ceiling.cu -o /tmp/p2p_ceiling && /tmp/p2p_ceiling
 #include <cstdio>
 #include <cstdint>
@@ -146,6 +146,54 @@ int main() {
     }
     printf("SM push v4 U8 both directions         grid %4d x 512  %7.1f + %7.1f GB/s\n", g,
            gb / (best[0] / 1e3), gb / (best[1] / 1e3));
+  }
+  // (6) both directions at once, pulled: GPU1 loads GPU0's memory and GPU0 loads
+  // GPU1's, each storing locally (the pull placement in the pairs topology)
+  for (int g : {148, 296, 444}) {
+    cudaStream_t st[2];
+    cudaEvent_t a[2], b[2];
+    for (int dv = 0; dv < 2; dv++) {
+      cudaSetDevice(dv); cudaStreamCreate(&st[dv]); cudaEventCreate(&a[dv]); cudaEventCreate(&b[dv]);
+    }
+    float best[2] = {1e30f, 1e30f};
+    for (int r = 0; r < 5; r++) {
+      for (int dv = 0; dv < 2; dv++) { cudaSetDevice(dv); cudaDeviceSynchronize(); }
+      for (int dv = 0; dv < 2; dv++) {
+        cudaSetDevice(dv);
+        cudaEventRecord(a[dv], st[dv]);
+        copy_k<1, 8, true><<<g, 512, 0, st[dv]>>>((const uint4*)(dv ? s0 : s1), (uint4*)(dv ? d1 : d0), bytes / 16);
+        cudaEventRecord(b[dv], st[dv]);
+      }
+      for (int dv = 0; dv < 2; dv++) {
+        cudaSetDevice(dv); cudaEventSynchronize(b[dv]);
+        float ms; cudaEventElapsedTime(&ms, a[dv], b[dv]); if (r && ms < best[dv]) best[dv] = ms;
+      }
+    }
+    printf("SM pull v4 U8 both directions         grid %4d x 512  %7.1f + %7.1f GB/s\n", g,
+           gb / (best[0] / 1e3), gb / (best[1] / 1e3));
+  }
+  // (7) both directions by the copy engines
+  {
+    cudaStream_t st[2];
+    cudaEvent_t a[2], b[2];
+    for (int dv = 0; dv < 2; dv++) {
+      cudaSetDevice(dv); cudaStreamCreate(&st[dv]); cudaEventCreate(&a[dv]); cudaEventCreate(&b[dv]);
+    }
+    float best[2] = {1e30f, 1e30f};
+    for (int r = 0; r < 6; r++) {
+      for (int dv = 0; dv < 2; dv++) { cudaSetDevice(dv); cudaDeviceSynchronize(); }
+      for (int dv = 0; dv < 2; dv++) {
+        cudaSetDevice(dv);
+        cudaEventRecord(a[dv], st[dv]);
+        cudaMemcpyPeerAsync(dv ? d0 : d1, dv ? 0 : 1, dv ? s1 : s0, dv, bytes, st[dv]);
+        cudaEventRecord(b[dv], st[dv]);
+      }
+      for (int dv = 0; dv < 2; dv++) {
+        cudaSetDevice(dv); cudaEventSynchronize(b[dv]);
+        float ms; cudaEventElapsedTime(&ms, a[dv], b[dv]); if (r && ms < best[dv]) best[dv] = ms;
+      }
+    }
+    printf("CE both directions                              %7.1f + %7.1f GB/s\n", gb / (best[0] / 1e3), gb / (best[1] / 1e3));
   }
   printf("done\n");
   return 0;
