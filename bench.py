@@ -516,8 +516,8 @@ def bench_c2(args):
                                    "two kernels on this GPU (ring_probe_rtt, system scope)"},
         "kernels_ms": {"put_avg": round(put_avg_ms, 5), "consume_avg": round(statistics.mean(get_ms), 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("r02_ncu_put_c2.json"),
-                     "traffic_source": "profiles/r02_ncu_put_c2.json (ncu --set full, put_kernel, same config)",
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("r02b_ncu_put_c2.json"),
+                     "traffic_source": "profiles/r02b_ncu_put_c2.json (ncu --set full, put_kernel, same config)",
                      "kernel": "put_kernel<0> (persistent engine: time per batch = step time)" if engine
                      else "put_kernel<0> (CUDA-event average per launch)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src_kind})",
@@ -1084,8 +1084,15 @@ def main():
                     if v is not None:
                         out[k] = v
                 if out.get("c3_one_way"):
+                    ce1 = (out.get("nvlink_ce") or {}).get("one_direction_gbs")
+                    for r in out["c3_one_way"].values():
+                        r["nvlink_frac_of_ce_one_way"] = round(r["value"] / ce1, 4) if ce1 else None
                     best = max(out["c3_one_way"].values(), key=lambda r: r["value"] if r["ok"] else 0)
                     out["c3_one_way"]["best"] = best["placement"]
+                    out["c3_one_way"]["what"] = (
+                        "north-star target (>= 80 % of 900 GB/s per direction, >= 4 MB messages) on ONE ring; "
+                        "split: the consumer's copy-out pulls over NVLink (1.125 wire bytes per payload byte, "
+                        "profiles/r02b_ncu_split_counters.csv), push: peer stores (1.21)")
         if out:
             print(json.dumps(out), flush=True)
     finally:
