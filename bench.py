@@ -834,7 +834,8 @@ def bench_c3_one_way(args, rank, world, grp, placement: str):
     if rank == 1:
         R.ring_bind_mirror(ring, 0, mhs[0])
     res = torch.zeros(4, dtype=torch.float64)
-    if rank in (0, 1):
+    active = rank in (0, 1)          # every rank walks the same collectives; ranks >= 2 do no work
+    if active:
         s = torch.cuda.Stream()
         if rank == 0:
             src = torch.empty(K * stride, dtype=torch.uint8, device="cuda")
@@ -853,7 +854,8 @@ def bench_c3_one_way(args, rank, world, grp, placement: str):
         for _ in range(warm):
             run()
         torch.cuda.synchronize()
-        dist.barrier(group=grp)
+    dist.barrier(group=grp)
+    if active:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         for _ in range(launches):
