@@ -1152,6 +1152,9 @@ static ring_status_t get_common(ring_t r, uint32_t n, ring_view_t* d_views, void
   a.sys = r->sys;
   a.n_mirrors = r->max_producers;
   a.remote_data = r->remote_data;
+  // B200RING_COPYOUT_ALIGN=1 / 0 forces the line-aligned copy-out loads on / off
+  // (tests exercise the remote path on one GPU; A/B measurements)
+  if (const char* e = getenv("B200RING_COPYOUT_ALIGN")) a.remote_data = e[0] == '1';
   DevGuard g(r->device);
   uint32_t ctas = r->copy_ctas, thr = r->threads, chunk = r->chunk;
   default_grid(r->device, false, &ctas, &thr, &chunk);

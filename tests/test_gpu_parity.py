@@ -101,6 +101,29 @@ def test_c1_stream_bit_exact(R, mode, copy_mode):
     assert all(int(v["t_visible"]) > 0 for v in views)
 
 
+@pytest.mark.parametrize("shape", ["c1", "wide", "c3"])
+def test_copyout_line_aligned_loads(R, monkeypatch, shape):
+    """The copy-out path for a buffer region on another GPU (split / pull),
+    forced on one GPU: units after an entry's first start on the source's
+    128-B lines, the first unit's lanes in front of the payload load the
+    header's line and store nothing, ragged last units keep 4 loads in flight
+    (DESIGN.md §6.2).  Sizes below 1 KiB, every ragged tail length class,
+    multi-unit entries and the C3 tensors; bit-exact against the oracle."""
+    monkeypatch.setenv("B200RING_COPYOUT_ALIGN", "1")
+    if shape == "c1":
+        L, stream = Layout(32768, 8), synth.random_stream(synth.SEED_BASE + 1, 0, 1000, 1, 4096)
+    elif shape == "wide":
+        L, stream = Layout(4 << 20, 32), synth.random_stream(synth.SEED_BASE + 11, 0, 300, 1000, 300000)
+    else:
+        L, stream = Layout(64 << 20, 64), synth.wan_stream(synth.SEED_BASE + 3, 0, 24)
+    sim = oracle_spsc(L, to_oracle_msgs(stream))
+    views, payloads, st, img = _run_spsc(R, L, stream, local=False)
+    assert st == [0] * len(stream)
+    check_views_against_oracle(views, sim, 0, stream)
+    assert payloads == [m.payload.tobytes() for m in stream]
+    assert img["tail"] == sim.mem.tail == img["head"]
+
+
 def test_c1_system_scope_same_device(R):
     """The same stream through a ring created without RING_CREATE_LOCAL (sys-scope fences)."""
     L = Layout(32768, 8)
