@@ -304,6 +304,11 @@ def bench_c2(args):
     clk.start()
     l0 = R.ring_launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the put kernel's average launch duration, live over the timed region: CUDA
+    # events on its own stream sp around the whole loop (sp carries only the
+    # put launches, back to back; events between launches would break the
+    # back-to-back launch and cost ~2-3 us each)
+    sp_start, sp_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sync()
     main = torch.cuda.current_stream()
     t_start.record(main)
@@ -313,8 +318,10 @@ def bench_c2(args):
     else:
         sp.wait_stream(main)
         sc.wait_stream(main)
+        sp_start.record(sp)
         for i in range(steps):
             step(args.warmup + i)
+        sp_end.record(sp)
         if engine:
             R.ring_peer_engine_wait(peer, sp)
         main.wait_stream(sp)
@@ -417,7 +424,15 @@ def bench_c2(args):
     put_bytes = m * (plen + f)                 # read s, write f per message
     # engine: one resident put grid; its time per batch in the stream IS the step
     # (the events around a doorbell would only time the doorbell)
-    put_avg_ms = (ms / args.steps) if engine else statistics.mean(put_ms)
+    if engine:
+        put_avg_ms = ms / args.steps
+        put_avg_src = "engine: timed region / steps"
+    elif graph is None:
+        put_avg_ms = sp_start.elapsed_time(sp_end) / args.steps
+        put_avg_src = f"CUDA events on the put stream around the {args.steps} put launches of the timed region"
+    else:
+        put_avg_ms = statistics.mean(put_ms)
+        put_avg_src = "CUDA events around 64 put launches of a separate eager pass (graph mode)"
     peaks, src_kind = load_peaks()
     achieved = put_bytes / (put_avg_ms / 1e3) / 1e9
 
@@ -514,12 +529,15 @@ def bench_c2(args):
                                    "the put publishes a run of complete entries with one fence, so a batch "
                                    "exceeds it by the run length.  t_RTT = median in-run flag round trip between "
                                    "two kernels on this GPU (ring_probe_rtt, system scope)"},
-        "kernels_ms": {"put_avg": round(put_avg_ms, 5), "consume_avg": round(statistics.mean(get_ms), 5)},
+        "kernels_ms": {"put_avg": round(put_avg_ms, 5), "put_avg_source": put_avg_src,
+                       "put_avg_events_per_launch": round(statistics.mean(put_ms), 5),
+                       "consume_avg": round(statistics.mean(get_ms), 5)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("r02b_ncu_put_c2.json"),
                      "traffic_source": "profiles/r02b_ncu_put_c2.json (ncu --set full, put_kernel, same config)",
                      "kernel": "put_kernel<0> (persistent engine: time per batch = step time)" if engine
-                     else "put_kernel<0> (CUDA-event average per launch)",
+                     else "put_kernel<0> (average launch duration on its stream over the timed region; "
+                          "ncu launch list: put 66 % of kernel time, profiles/r02b_ncu_launches_c2.json)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src_kind})",
                      "algorithmic_bytes_per_launch": put_bytes},
         "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": m * stride,
