@@ -292,8 +292,18 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
     // align_src: units after the first start on the source's 128-B lines (the
     // first is `sh` bytes short; the control warp planned units_for(len + sh))
     const uint32_t sh = align_src ? (uint32_t)(src & 127u) : 0u;
-    const uint64_t lo = c ? (uint64_t)c * chunk - sh : 0;
-    const uint64_t hi = min(len, (uint64_t)(c + 1) * chunk - sh);
+    uint64_t lo = c ? (uint64_t)c * chunk - sh : 0;
+    uint64_t hi = min(len, (uint64_t)(c + 1) * chunk - sh);
+#ifndef B200RING_RAGGED_FIRST
+#define B200RING_RAGGED_FIRST 1
+#endif
+    if (B200RING_RAGGED_FIRST && !align_src && nu_hit > 1) {
+      // the ragged part of an item is its FIRST unit, so the units a launch
+      // hands out last are whole ones
+      const uint64_t rag = len - (uint64_t)(nu_hit - 1) * chunk;
+      lo = c ? rag + (uint64_t)(c - 1) * chunk : 0;
+      hi = c ? rag + (uint64_t)c * chunk : rag;
+    }
     if (tr && lane == 0) tr[2] = globaltimer();
     RING_CHECK(c < (uint32_t)((len + sh + chunk - 1) / chunk) || len == 0, "unit inside its item", u, item);
     if (hi > lo)
