@@ -1023,7 +1023,7 @@ def reference_arm(args):
         per, Rb, N, wl = 64, 64 << 20, 64, "C2 sample: 64 x 1,048,512-B messages per step (one ring's worth)"
     else:
         lo, hi = C3_LENS[1], C3_LENS[0]
-        per, Rb, N, wl = 16, 64 << 20, 64, "C3 sample: 16 x ~4 MiB messages per step"
+        per, Rb, N, wl = 128, 256 << 20, 64, "C3 sample: 128 x ~4 MiB messages per step (one pair launch's worth)"
     times, nbytes, res = [], 0, None
     for i in range(args.warmup + args.steps):
         res = T.run(Rb, N, 1, per, lo, hi, 20260120 + i)
