@@ -142,6 +142,81 @@ def test_c2_bench_streaming_loop(R, mode):
 
 
 # ---------------------------------------------------------------------------------------
+# C3 one way: bench.py's c3_one_way split loop
+# ---------------------------------------------------------------------------------------
+@CROSS
+def test_c3_split_one_way_bench_loop(R, monkeypatch, cross):
+    """BASELINE.json configs[2] in bench.py's c3_one_way launch configuration
+    (the north-star target's ring): split placement, 256 MiB / 64 slots, 64
+    Wan2.1 tensors (4,194,304 / 4,193,280 B alternating) per put launch and per
+    copy-out consume launch, producer and consumer on their own streams, 4
+    launches (the ring wraps with PAD entries).  Every placement and header
+    against the oracle's pointer formulas, every payload in the copy-out
+    buffers compared on the device.  On one GPU the line-aligned copy-out of a
+    remote buffer region is forced (B200RING_COPYOUT_ALIGN=1)."""
+    prod, cons = devices(2, cross)
+    if not cross:
+        monkeypatch.setenv("B200RING_COPYOUT_ALIGN", "1")
+    L = Layout(256 << 20, 64)
+    K, launches = 64, 4
+    seed = synth.SEED_BASE + 33
+    lens_k = [EMB if q % 2 == 0 else LAT480 for q in range(K)]
+    ring = R.ring_create_split(cons, prod, L.R, L.N, 1, 0)
+    peer, mh = R.ring_attach_peer(R.ring_export(ring), prod, 0)
+    R.ring_bind_mirror(ring, 0, mh)
+    with torch.cuda.device(prod):
+        buf, ptrs = device_sources([(0, k, lens_k[k]) for k in range(K)], seed, f"cuda:{prod}")
+        hdrs = [synth.header_fields(seed, 0, k) for k in range(K)]
+        d_msgs = _msgs(R, ptrs, lens_k, hdrs, 7, 2, f"cuda:{prod}")
+        sts = [torch.full((K,), 10, dtype=torch.int32, device=f"cuda:{prod}") for _ in range(launches)]
+        sp = torch.cuda.Stream(prod)
+    with torch.cuda.device(cons):
+        vts = [torch.zeros(K * 128, dtype=torch.uint8, device=f"cuda:{cons}") for _ in range(launches)]
+        dsts = [torch.empty(K * EMB, dtype=torch.uint8, device=f"cuda:{cons}") for _ in range(2)]
+        dptr = [dev_u64([d.data_ptr() + q * EMB for q in range(K)]) for d in dsts]
+        dlens = dev_u64(lens_k)
+        chans = torch.zeros(K, dtype=torch.int32, device=f"cuda:{cons}")
+        keys = dev_u64(list(range(K)))
+        sc = torch.cuda.Stream(cons)
+        # load the verifier on the consumer's GPU now: a first (lazy) load would
+        # wait for the consume kernel spinning there (DESIGN.md §6.4)
+        SD.verify(dptr[0][:1], dlens[:1], chans[:1], keys[:1], seed)
+        torch.cuda.synchronize(cons)
+    bads = []
+    try:
+        for i in range(launches):
+            R.ring_consume(ring, K, vts[i], dsts[i % 2], EMB, 0, sc)
+            with torch.cuda.device(cons):
+                bads.append(SD.verify(dptr[i % 2], dlens, chans, keys, seed, sc))
+            R.ring_put_batch(peer, d_msgs, K, 0, sts[i], sp)
+        for d in {prod, cons}:
+            torch.cuda.synchronize(d)
+        img = spsc_image(L, lens_k * launches)
+        ents = [e for e in img["entries"] if not e[3]]
+        assert any(e[3] for e in img["entries"])                  # the ring wrapped with a PAD
+        for i in range(launches):
+            assert sts[i].cpu().tolist() == [0] * K, (i, sts[i].cpu().tolist())
+            v = views_host(vts[i])
+            for q in range(K):
+                k = i * K + q
+                assert int(v[q]["status"]) == 0, (k, int(v[q]["status"]))
+                assert _place(v[q]) == ents[k][1:3] + (ents[k][0],), k
+                h = hdrs[q]
+                exp = encode_header(h[0], h[1], 7, 2, lens_k[q], 0, k, 0, 0, 0)[:56]
+                assert bytes(v[q]["header"])[:56] == exp, k
+                assert int(v[q]["len"]) == lens_k[q]
+        for j, b in enumerate(bads):
+            _ok(b, j)
+        im = R.ring_read_image(ring)
+        assert im["tail"] == img["tail"] == im["head"] == im["cursor"]
+    finally:
+        for d in {prod, cons}:
+            torch.cuda.synchronize(d)
+        R.ring_detach(peer)
+        R.ring_destroy(ring)
+
+
+# ---------------------------------------------------------------------------------------
 # C4: the Wan2.1 I2V stage chain
 # ---------------------------------------------------------------------------------------
 C4_HOPS = [  # (R, N, message bytes): text-enc -> VAE-enc -> DiT -> VAE-dec -> sink
