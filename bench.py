@@ -706,6 +706,22 @@ def bench_pairs(args, rank, world, grp):
     _, v = latencies()
     ok = bool((status == 0).all().item()) and bool((v["status"] == 0).all())
     log(f"timed region {ms:.3f} ms, ok = {ok}")
+    # sampled payload check: 4 messages of the last timed step, byte for byte
+    # against the producer's seeded tensors (push: in the ring, released but
+    # not yet overwritten -- the step's last 32 messages, the ring holds 63;
+    # pull / split: in the copy-out buffer)
+    last, prev_r = args.warmup + args.steps - 1, (rank - 1) % world
+    mism, sampled = 0, 0
+    for q in sorted({max(0, m - 32), max(0, m - 16), max(0, m - 2), m - 1}):
+        k = (last % sets) * m + q
+        shape, distn = synth.WAN_SHAPES[("umt5_emb", "latent_480p")[k % 2]]
+        exp = synth.bf16_tensor_bytes(synth.SEED_BASE + 3, prev_r, k, shape, distn).tobytes()
+        n = int(v[q]["len"])
+        got = (pull_dst[q * stride: q * stride + n].cpu().numpy().tobytes() if pull
+               else R.ring_read_data(ring, int(v[q]["offset"]), n))
+        sampled += 1
+        mism += int(got != exp)
+    ok = ok and mism == 0
     # loaded latency pooled over further streamed steps (outside the timed
     # region), one view buffer per step, first 10 % dropped
     lat_steps = 20
@@ -764,7 +780,7 @@ def bench_pairs(args, rank, world, grp):
     summary = torch.tensor([ms, e2e_ms, 0.0 if ok else 1.0, float(launches)], dtype=torch.float64)
     dist.all_reduce(summary, op=dist.ReduceOp.MAX, group=grp)
     gathered = [None] * world
-    dist.all_gather_object(gathered, (lat_loaded, unl[4096], unl[C3_LENS[0]]), group=grp)
+    dist.all_gather_object(gathered, (lat_loaded, unl[4096], unl[C3_LENS[0]], mism, sampled), group=grp)
     cpu = None
     ce, rtt = None, None
     if rank == 0:
@@ -813,6 +829,9 @@ def bench_pairs(args, rank, world, grp):
                    "l2": f"inputs larger than L2 per rank (2 x {m * 4} MiB source sets)",
                    "parallelism": f"{world} concurrent SPSC rings (one egress + one ingress stream per GPU)"},
         "per_gpu_gbs": round(per_gpu, 2),
+        "verified": {"sampled_messages": sum(g[4] for g in gathered), "payload_mismatches": sum(g[3] for g in gathered),
+                     "what": "per rank, 4 messages of the last timed step compared byte for byte with the "
+                             "producer's seeded Wan2.1 tensors (synth.bf16_tensor_bytes)"},
         # forward bytes on the link per message = footprint +
         # size slot + tail word (the ncu counters add the link protocol on top:
         # profiles/r02_ncu_nvlink_counters.csv, 1.21 wire bytes per payload byte)
