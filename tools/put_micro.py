@@ -15,7 +15,7 @@ src = torch.randint(0, 255, (256 << 20,), dtype=torch.uint8, device="cuda")
 views = torch.zeros(64 * 128, dtype=torch.uint8, device="cuda")
 status = torch.zeros(64, dtype=torch.int32, device="cuda")
 cases = [("64 x 0 B", 64, 0), ("64 x 4 KiB", 64, 4096), ("63 x 1 MiB-64", 63, 1048512),
-         ("15 x 4 MiB-64", 15, 4194240)]
+         ("15 x 4 MiB-64", 15, 4194240), ("1 x 4 KiB", 1, 4096)]
 TRACE = bool(os.environ.get("B200RING_TRACE"))
 if os.environ.get("CASES"):
     cases = [cases[int(c)] for c in os.environ["CASES"].split(",")]
