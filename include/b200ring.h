@@ -405,6 +405,16 @@ ring_status_t ring_peer_trace(ring_peer_t peer, uint64_t* host_out, uint32_t n);
 ring_status_t ring_get_trace(ring_t ring, uint64_t* host_out, uint32_t n);
 ring_status_t ring_write_data(ring_t ring, uint64_t offset, uint64_t len, const void* host_src);
 
+/* ---- environment knobs (read by the host at each launch; for experiments and tests)
+ *   B200RING_TRACE=1          debug timelines (ring_peer_trace, ring_get_trace)
+ *   B200RING_CHUNK=<bytes>    copy unit size, power of two 4 KiB .. 1 MiB (default
+ *                             16 KiB for NVLink destinations, 32 KiB otherwise)
+ *   B200RING_CARVEOUT=<pct>   shared-memory carveout of every ring kernel (default 8:
+ *                             kernels of one carveout co-reside on an SM)
+ *   B200RING_COPYOUT_ALIGN=0|1  force the copy-out loads on the source's 128-B lines
+ *                             off / on (default: on iff the buffer region is on another
+ *                             GPU -- ring_open, ring_create_split) */
+
 /* ---- stage router (PAPER.md:524-532 round-robin ResultDeliver; PAPER.md:914-924
  * NodeManager reassignment, mechanism only) ------------------------------------------
  * A device-resident route table on the producer GPU: for each (app_id, stage)
