@@ -1,16 +1,17 @@
 """Reserve-then-commit MPSC rings (oracle/reserve.py):
 producers on concurrent streams (and across GPUs when available) claim under
 the lock and copy outside it, with a consumer running concurrently.  Every
-channel is delivered exactly once, in order, byte-exact; the ring's placement
-equals the fault-free oracle's for the observed claim order (claims are
-serialised under the lock, so the entries tile the ring exactly as one
-producer's stream with the merged lengths would: PAPER.md:731-745, R3)."""
+channel is delivered exactly once, in order, byte-exact; the entries tile the
+ring by the pointer formulas (R3) -- as one producer's
+stream with the merged lengths would, except that a PAD reserved by a sender
+that then waits for credit without the lock (R23) may precede another
+sender's smaller message."""
 import numpy as np
 import pytest
 
 import synth
 from gpu_util import msg_tensor, upload, views_host
-from oracle.ring import Layout, decode_header, spsc_image
+from oracle.ring import Layout, decode_header, footprint, seq_next, spsc_image
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -68,9 +69,32 @@ def test_reserve_commit_concurrent_producers(R, cross):
     for j, (x, hd) in enumerate(zip(v, hs)):
         m = streams[hd["producer_id"]][hd["seq"]]
         assert out[j * cap: j * cap + int(x["len"])].tobytes() == m.payload.tobytes()
+    # Placement: the pointer formulas over the observed entries.
+    # A PAD here may belong to a sender that reserved it and then waited for
+    # credit WITHOUT the lock (reserve-then-commit, R23; oracle/reserve.py:
+    # ClaimPad, then UnlockFull -> AdvW / RH) while another sender's smaller
+    # message went in after it, so the PADs are where the GPU put them:
+    # each one fills [end of the previous entry, R) and is needed by a message
+    # of a waiting sender (one of the next max_producers entries does not fit).
+    ent = [(int(x["slot_seq"]), int(x["start"]), int(x["footprint"])) for x in v]
+    assert [e[2] for e in ent] == [footprint(L, int(x["len"])) for x in v]
+    pos = 0
+    for q, (sq, st, f) in enumerate(ent):
+        if q and sq == seq_next(seq_next(ent[q - 1][0])):   # one PAD slot in between: [pos, R), then 0
+            assert pos < L.R and st == 0, (q, pos, st)
+            assert any(e[2] > L.R - pos for e in ent[q:q + 3]), (q, pos)
+        else:
+            assert q == 0 or sq == seq_next(ent[q - 1][0]), (q, sq, ent[q - 1][0])
+            assert st == (pos if pos < L.R else 0), (q, st, pos)
+        pos = st + f
+    # unless such a PAD went in ahead of a message that fits, the placement is
+    # exactly the SPSC rule over the merged order
+    early_pad = any(ent[q][0] == seq_next(seq_next(ent[q - 1][0])) and
+                    ent[q][2] <= L.R - (ent[q - 1][1] + ent[q - 1][2]) for q in range(1, len(ent)))
     merged = [streams[hd["producer_id"]][hd["seq"]].length for hd in hs]
     img = [e for e in spsc_image(L, merged)["entries"] if not e[3]]
-    assert [(int(x["slot_seq"]), int(x["start"]), int(x["footprint"])) for x in v] == [tuple(e[:3]) for e in img]
+    if not early_pad:
+        assert ent == [tuple(e[:3]) for e in img]
     im = R.ring_read_image(ring)
     assert im["lock"] == 0 and im["tail"] == im["head"]
     for pe in peers:
