@@ -488,7 +488,7 @@ def bench_c2(args):
     # the same with the persistent put engine feeding the ring (one resident put
     # grid: the next batch's copies overlap the current batch's copy-out)
     co_engine, co_eng_ms, co_eng_ok = None, None, None
-    if not engine:
+    if not engine and not args.copy_mode:      # (the engine drives LSU copy warps only)
         R.ring_peer_engine_start(peer, sp)
         for i in range(3):
             R.ring_put_batch(peer, d_msgs[i % sets], m, 0, status, sp)

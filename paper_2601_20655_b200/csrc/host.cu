@@ -968,7 +968,8 @@ static ring_status_t put_common(ring_peer_t p, const ring_msg_t* d_msgs, const r
   default_grid(p->device, p->device != p->data_device, &ctas, &thr, &chunk);
   a.copy_mode = p->copy_mode;
   // engine stages live in shared memory: the largest power of two that fits
-  while (a.copy_mode == 1 && chunk > 4096 && (uint64_t)chunk * kEngineStages > kEngineSmem) chunk >>= 1;
+  while (a.copy_mode == 1 && chunk > 4096 && (uint64_t)chunk * kEngineStages * kMaxEngineWarps > kEngineSmem)
+    chunk >>= 1;
   a.chunk = chunk;
   a.launch = p->launches;
   if (getenv("B200RING_TRACE")) {

@@ -1289,13 +1289,19 @@ __global__ void __maxnreg__(96) put_kernel(const __grid_constant__ PutArgs a) {
     }
   }
   __shared__ SpecRound spec;
-  if (MODE == 1) {             // TMA engine: one warp per CTA (CTA 0: warp 2); it evaluates the first round itself
+  if (MODE == 1) {
+    // TMA engines: every warp of the CTA but CTA 0's two control warps drives
+    // its own ring of kEngineStages shared-memory stages (a warp blocks while
+    // it waits for a store to complete before its arrive; the others keep
+    // their copies in flight).  The first engine warp evaluates the first round.
     extern __shared__ __align__(128) uint8_t dyn_smem[];
-    if (warp == (blockIdx.x == 0 ? 2 : 0)) {
-      spec_first_round(a, &spec);
-      __syncwarp();
-      copy_engine<kEngineStages>(ctx, S, a.chunk, a.timeout_ns, dyn_smem, &spec);
-    }
+    const int ew = warp - (blockIdx.x == 0 ? 2 : 0);
+    const int n_ew = min((int)(blockDim.x >> 5) - (blockIdx.x == 0 ? 2 : 0), kMaxEngineWarps);
+    if (ew < 0 || ew >= n_ew) return;
+    if (ew == 0) spec_first_round(a, &spec);
+    asm volatile("bar.sync 3, %0;" ::"r"(n_ew * 32) : "memory");
+    copy_engine<kEngineStages>(ctx, S, a.chunk, a.timeout_ns, dyn_smem + (size_t)ew * kEngineStages * a.chunk, &spec,
+                               ew);
     return;
   }
   // the CTA's first copy warp evaluates the first round; the copy warps meet
@@ -1402,8 +1408,8 @@ cudaError_t launch_engine_wait(EngineQueue* q, uint64_t upto, uint64_t timeout_n
 }
 
 cudaError_t launch_put(const PutArgs& a, uint32_t ctas, uint32_t threads, cudaStream_t s) {
-  const size_t dyn = a.copy_mode == 1 ? (size_t)kEngineStages * a.chunk : 0;
-  if (a.copy_mode == 1) put_kernel<1><<<ctas, 96u, dyn, s>>>(a);
+  const size_t dyn = a.copy_mode == 1 ? (size_t)kMaxEngineWarps * kEngineStages * a.chunk : 0;
+  if (a.copy_mode == 1) put_kernel<1><<<ctas, 32u * (kMaxEngineWarps < 3 ? 3 : kMaxEngineWarps), dyn, s>>>(a);
   else if (a.dest0.sys && !a.routes) put_kernel<2><<<ctas, threads, 0, s>>>(a);
   else put_kernel<0><<<ctas, threads, 0, s>>>(a);
   return cudaGetLastError();

@@ -409,11 +409,15 @@ __device__ __forceinline__ void bulk_wait_group_read(uint32_t allow) {   // thei
 // stores outstanding).
 template <int STAGES>
 __device__ void copy_engine(LaunchCtx* ctx, LaunchSet* S, uint32_t chunk, uint64_t timeout_ns, uint8_t* bufs,
-                            const SpecRound* spec = nullptr) {
+                            const SpecRound* spec = nullptr, int ew = 0) {
   const int lane = threadIdx.x & 31;
-  __shared__ __align__(8) uint64_t bar[STAGES];
-  __shared__ EngineStage st[STAGES];
-  __shared__ uint32_t items[2 * STAGES];    // item of unit k (k_issue - k_done <= 2 STAGES)
+  // per engine warp `ew` of the CTA: its own stages, barriers and bookkeeping
+  __shared__ __align__(8) uint64_t bar_all[kMaxEngineWarps][STAGES];
+  __shared__ EngineStage st_all[kMaxEngineWarps][STAGES];
+  __shared__ uint32_t items_all[kMaxEngineWarps][2 * STAGES];   // item of unit k (k_issue - k_done <= 2 STAGES)
+  uint64_t* bar = bar_all[ew];
+  EngineStage* st = st_all[ew];
+  uint32_t* items = items_all[ew];
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])) : "memory");

@@ -239,6 +239,10 @@ struct PutArgs {
 #endif
 constexpr int kEngineStages = B200RING_ENGINE_STAGES;   // TMA engine: shared-memory stages of `chunk` bytes
 constexpr uint32_t kEngineSmem = 200u << 10;             // dynamic shared memory the stages may use
+#ifndef B200RING_ENGINE_WARPS
+#define B200RING_ENGINE_WARPS 3
+#endif
+constexpr int kMaxEngineWarps = B200RING_ENGINE_WARPS;    // TMA engine warps per CTA (CTA 0: one)
 
 struct GetArgs {
   uint8_t* ring;
