@@ -235,12 +235,12 @@ struct PutArgs {
 };
 
 #ifndef B200RING_ENGINE_STAGES
-#define B200RING_ENGINE_STAGES 4
+#define B200RING_ENGINE_STAGES 2
 #endif
 constexpr int kEngineStages = B200RING_ENGINE_STAGES;   // TMA engine: shared-memory stages of `chunk` bytes
 constexpr uint32_t kEngineSmem = 200u << 10;             // dynamic shared memory the stages may use
 #ifndef B200RING_ENGINE_WARPS
-#define B200RING_ENGINE_WARPS 3
+#define B200RING_ENGINE_WARPS 6
 #endif
 constexpr int kMaxEngineWarps = B200RING_ENGINE_WARPS;    // TMA engine warps per CTA (CTA 0: one)
 
