@@ -871,7 +871,7 @@ def bench_pairs(args, rank, world, grp):
     }
 
 
-def bench_c3_one_way(args, rank, world, grp, placement: str):
+def bench_c3_one_way(args, rank, world, grp, placement: str, put_cfg=None):
     """BASELINE.json configs[2] as the north star states its target: ONE ring,
     GPU 0 -> GPU 1, 4-MB Wan2.1 tensors, GB/s per direction against 900.
     placement "split" (ring_create_split, R28: control words and header copies
@@ -900,6 +900,8 @@ def bench_c3_one_way(args, rank, world, grp, placement: str):
     mh = None
     if rank == 0:
         peer, mh = R.ring_attach_peer(hs[1], dev, 0)
+        if put_cfg:                       # (ctas, threads, copy_mode): e.g. the TMA engine on 17 SMs
+            R.ring_peer_config(peer, *put_cfg)
     mhs = [None] * world
     dist.all_gather_object(mhs, mh, group=grp)
     if rank == 1:
@@ -960,7 +962,8 @@ def bench_c3_one_way(args, rank, world, grp, placement: str):
         return None
     ms = max(out[0][0], out[1][0])
     gbs = sum(lens) * launches / (ms / 1e3) / 1e9
-    return {"placement": placement, "value": round(gbs, 1), "unit": "GB/s (payload, one direction)",
+    return {"placement": placement, "put": ({"ctas": put_cfg[0], "copy_mode": put_cfg[2]} if put_cfg else "default"),
+            "value": round(gbs, 1), "unit": "GB/s (payload, one direction)",
             "nvlink_frac_of_900": round(gbs / NVLINK_NOMINAL, 4), "ms": round(ms, 3),
             "ms_producer": round(out[0][0], 3), "ms_consumer": round(out[1][0], 3),
             "ok": out[0][1] == 1.0 and out[1][1] == 1.0 and out[1][2] == 0.0,
@@ -1141,6 +1144,9 @@ def main():
             offsets = [None] * world
             dist.all_gather_object(offsets, R_clock_offset(local), group=grp)
             extra["c3_one_way"] = {pl: bench_c3_one_way(args, rank, world, grp, pl) for pl in ("split", "push")}
+            # the paper's L3 concern (transfers off the SMs): the push by
+            # the TMA engine on 17 SMs (no LSU copy)
+            extra["c3_one_way"]["push_tma_17sm"] = bench_c3_one_way(args, rank, world, grp, "push", (17, 0, 1))
             if world >= 4:
                 a4 = copy.copy(args)
                 a4.steps, a4.warmup, a4.msgs_per_step = 10, 3, 2
@@ -1160,12 +1166,13 @@ def main():
                     ce1 = (out.get("nvlink_ce") or {}).get("one_direction_gbs")
                     for r in out["c3_one_way"].values():
                         r["nvlink_frac_of_ce_one_way"] = round(r["value"] / ce1, 4) if ce1 else None
-                    best = max(out["c3_one_way"].values(), key=lambda r: r["value"] if r["ok"] else 0)
-                    out["c3_one_way"]["best"] = best["placement"]
+                    best = max(out["c3_one_way"].items(), key=lambda kv: kv[1]["value"] if kv[1]["ok"] else 0)
+                    out["c3_one_way"]["best"] = best[0]
                     out["c3_one_way"]["what"] = (
                         "north-star target (>= 80 % of 900 GB/s per direction, >= 4 MB messages) on ONE ring; "
                         "split: the consumer's copy-out pulls over NVLink (1.125 wire bytes per payload byte, "
-                        "profiles/r02b_ncu_split_counters.csv), push: peer stores (1.21)")
+                        "profiles/r02b_ncu_split_counters.csv), push: peer stores (1.21), push_tma_17sm: the "
+                        "same push by the TMA engine on 17 SMs (6 engine warps per CTA, no LSU copy)")
         if out:
             print(json.dumps(out), flush=True)
     finally:
