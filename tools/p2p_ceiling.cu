@@ -195,6 +195,30 @@ int main() {
     }
     printf("CE both directions                              %7.1f + %7.1f GB/s\n", gb / (best[0] / 1e3), gb / (best[1] / 1e3));
   }
+  // (8) both directions driven from ONE GPU: GPU0 pushes 0 -> 1 and pulls 1 -> 0
+  //     at the same time (two kernels, two streams, g CTAs each)
+  for (int g : {74, 148}) {
+    cudaStream_t st2[2];
+    cudaEvent_t a2[2], b2[2];
+    CK(cudaSetDevice(0));
+    for (int k = 0; k < 2; k++) { cudaStreamCreate(&st2[k]); cudaEventCreate(&a2[k]); cudaEventCreate(&b2[k]); }
+    float best[2] = {1e30f, 1e30f};
+    for (int r = 0; r < 5; r++) {
+      cudaDeviceSynchronize();
+      cudaEventRecord(a2[0], st2[0]);
+      copy_k<1, 8, true><<<g, 512, 0, st2[0]>>>((const uint4*)s0, (uint4*)d1, bytes / 16);   // push 0 -> 1
+      cudaEventRecord(b2[0], st2[0]);
+      cudaEventRecord(a2[1], st2[1]);
+      copy_k<1, 8, true><<<g, 512, 0, st2[1]>>>((const uint4*)s1, (uint4*)d0, bytes / 16);   // pull 1 -> 0
+      cudaEventRecord(b2[1], st2[1]);
+      for (int k = 0; k < 2; k++) {
+        cudaEventSynchronize(b2[k]);
+        float ms; cudaEventElapsedTime(&ms, a2[k], b2[k]); if (r && ms < best[k]) best[k] = ms;
+      }
+    }
+    printf("GPU0 push 0->1 + pull 1->0 at once   grid %4d x 512  %7.1f + %7.1f GB/s\n", g,
+           gb / (best[0] / 1e3), gb / (best[1] / 1e3));
+  }
   printf("done\n");
   return 0;
 }
