@@ -32,6 +32,8 @@ from paper_2601_20655_b200 import topology as T
 
 METRIC = "ring transfer GB/s per GPU vs 900 GB/s NVLink; p50/p99 msg latency at 1/2/4/8 GPU"
 NVLINK_PEAK_MEASURED = 770.0
+# one GPU's NVLink ingress fed by k GPUs' SM pushes at once (profiles/r02b_p2p_fanin.txt)
+FANIN_INGRESS = {1: 680.0, 2: 715.6, 3: 718.3}
 
 # Wan2.1 I2V intermediate tensors
 EMB = synth.wan_bytes("umt5_emb")                       # 4,194,304
@@ -282,8 +284,12 @@ def run_fanin(args, rank, world, grp, offsets):
                            "rc": "reserve-then-commit MPSC ring: claim under the lock, copy outside it",
                            "mpsc": "paper MPSC ring with the lock"}[mode],
             "producers": world - 1, "sweep": rows,
-            "roofline": {"bound": "nvlink (consumer ingress)", "achieved": best, "peak": NVLINK_PEAK_MEASURED,
-                         "frac": round(best / NVLINK_PEAK_MEASURED, 4)},
+            "roofline": {"bound": "nvlink (consumer ingress)", "achieved": best,
+                         "peak": FANIN_INGRESS.get(world - 1, NVLINK_PEAK_MEASURED),
+                         "frac": round(best / FANIN_INGRESS.get(world - 1, NVLINK_PEAK_MEASURED), 4),
+                         "peak_source": ("profiles/r02b_p2p_fanin.txt: bare SM pushes from the producers' GPUs into "
+                                         "one GPU at once (tools/p2p_fanin.cu)" if world - 1 in FANIN_INGRESS else
+                                         "B200_PROFILING.md peer copy 770 GB/s (no measured ingress for this fan-in)")},
             "config": {"workload": ("C5a variant (SURVEY.md sec 8 f3): GPUs 1..N-1 -> one 512 MiB SPSC ring each on GPU 0, "
                                     "one consumer warp" if lockfree else
                                     "C5a variant (SURVEY.md sec 8 f3 ii): GPUs 1..N-1 -> one reserve-then-commit MPSC "
