@@ -36,6 +36,8 @@ def nvlink():
     ring = R.ring_create(1, 1 << 30, 256, 1, 0)
     peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
     R.ring_bind_mirror(ring, 0, mh)
+    if os.environ.get("PUT_CFG"):       # ctas:threads:copy_mode, e.g. 17:0:1 = the TMA engine on 17 SMs
+        R.ring_peer_config(peer, *(int(x) for x in os.environ["PUT_CFG"].split(":")))
     m, size = 32, 4194304
     src = torch.randint(0, 255, (256 << 20,), dtype=torch.uint8, device="cuda:0")
     d = msgs(src, size, m, "cuda:0")
