@@ -890,7 +890,7 @@ def bench_c3_one_way(args, rank, world, grp, placement: str, put_cfg=None):
     from paper_2601_20655_b200 import ring as R
     from synth import device as SD
     dev = int(os.environ.get("LOCAL_RANK", rank))
-    Rb, N, K, launches, warm = 256 << 20, 64, 64, int(os.environ.get("B200RING_C3_LAUNCHES", 40)), 2
+    Rb, N, K, launches, warm = 256 << 20, 64, 64, int(os.environ.get("B200RING_C3_LAUNCHES", 120)), 2
     stride, seed = 4194304, synth_seed_c3()
     lens = [C3_LENS[q % 2] for q in range(K)]
     split = placement == "split"
