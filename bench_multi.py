@@ -111,9 +111,17 @@ def _verify_pass(ring, total, seed, stream):
     return nbad, order_ok and bool((vv["status"] == 0).all()), vv
 
 
-def _wire(plan, rank, world, grp, dev):
-    return T.wire(plan, rank, world, grp, device=dev,
-                  create=lambda s, d: R.ring_create(d, s.data_bytes, s.n_slots, s.max_producers, s.flags),
+def _wire(plan, rank, world, grp, dev, split=()):
+    """Rings named in `split` take the split placement (ring_create_split, R28):
+    control words at the consumer, buffer region on the producer's GPU -- the
+    consumer pulls every payload over NVLink with its copy-out.  The producer of
+    ring "hop{s}" is rank s (device s)."""
+    def create(s, d):
+        if s.name in split:
+            return R.ring_create_split(d, int(s.name[3:]) % torch.cuda.device_count(), s.data_bytes, s.n_slots,
+                                       s.max_producers, s.flags)
+        return R.ring_create(d, s.data_bytes, s.n_slots, s.max_producers, s.flags)
+    return T.wire(plan, rank, world, grp, device=dev, create=create,
                   export=R.ring_export, attach=R.ring_attach_peer, bind=R.ring_bind_mirror)
 
 
@@ -131,7 +139,11 @@ def run_pipeline(args, rank, world, grp, offsets):
     outs = (STAGE_OUT[:world - 1] + [FRAMES]) if world < 4 else STAGE_OUT + [EMB] * (world - 4)
     hop_bytes = [(1 << 30) if b >= (256 << 20) else (256 << 20) for b in outs]
     hop_slots = [8 if b >= (256 << 20) else 64 for b in outs]
-    wired = _wire(T.plan_pipeline(world, hop_bytes, hop_slots), rank, world, grp, dev)
+    # frames-sized hops (>= 256 MiB) pulled by their consumer (split placement):
+    # one way, pulls carry 1.125 wire bytes per payload byte against 1.21 for
+    # peer stores; the smaller hops stay pushed
+    split = {f"hop{s}" for s, b in enumerate(outs) if b >= (256 << 20)} if getattr(args, "c4_split", True) else set()
+    wired = _wire(T.plan_pipeline(world, hop_bytes, hop_slots), rank, world, grp, dev, split)
     B = args.msgs_per_step or 2
     out_bytes = outs[rank]
     src = _fill(out_bytes, 1000 + rank)
@@ -141,13 +153,19 @@ def run_pipeline(args, rank, world, grp, offsets):
     st = torch.zeros(B, dtype=torch.int32, device="cuda")
     vt = torch.zeros(B * 128, dtype=torch.uint8, device="cuda")
     s_put, s_get = torch.cuda.Stream(), torch.cuda.Stream()
+    in_name = f"hop{(rank - 1) % world}"
+    in_bytes = outs[(rank - 1) % world]
+    pulled = torch.empty(B * in_bytes, dtype=torch.uint8, device="cuda") if in_name in split else None
+
+    def consume():
+        R.ring_consume(in_ring, B, vt, pulled, in_bytes if pulled is not None else 0, 0, s_get)
 
     def step():
         if rank == 0:      # new requests enter; the sink drains independently
             R.ring_put_batch(peer, d_msgs, B, 0, st, s_put)
-            R.ring_consume(in_ring, B, vt, None, 0, 0, s_get)
+            consume()
         else:              # store-and-forward stage: receive the request, emit the next tensor
-            R.ring_consume(in_ring, B, vt, None, 0, 0, s_get)
+            consume()
             s_put.wait_stream(s_get)
             R.ring_put_batch(peer, d_msgs, B, 0, st, s_put)
 
@@ -188,7 +206,9 @@ def run_pipeline(args, rank, world, grp, offsets):
             "hop_latency_us": hop_lat,
             "e2e_transport_latency_p50_us": round(sum(h["p50"] for h in hop_lat.values() if h["p50"] is not None), 2),
             "config": {"workload": "C4 Wan2.1-I2V stage pipeline (store-and-forward per batch of requests)",
-                       "requests_per_step": B, "hop_ring_bytes": hop_bytes, "hop_slots": hop_slots},
+                       "requests_per_step": B, "hop_ring_bytes": hop_bytes, "hop_slots": hop_slots,
+                       "hop_placement": ["split (consumer pulls)" if f"hop{s}" in split else "push"
+                                         for s in range(world)]},
             "higher_is_better": True, "dtype": "u8", "data": "synthetic", "ok": ok == 1 and float(t[1]) == 0.0}
 
 

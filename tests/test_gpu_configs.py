@@ -228,19 +228,25 @@ C4_HOPS = [  # (R, N, message bytes): text-enc -> VAE-enc -> DiT -> VAE-dec -> s
 
 
 @CROSS
-def test_c4_stage_chain(R, cross):
+@pytest.mark.parametrize("frames", ["push", "split"])
+def test_c4_stage_chain(R, cross, frames):
     """BASELINE.json configs[3]: every stage gets its input (view, in place),
     checks it on the device, releases it and emits its own output (a seeded
     tensor of the next shape, keyed by the request) into the next hop; hops are
     system-scope rings (NVLink kernels), stages run concurrently on their own
     streams, four requests (two laps of the 1 GiB frames ring, whose producer
-    waits for the sink's credit)."""
+    waits for the sink's credit).  frames="split": the frames hop in bench.py's
+    placement -- a split ring whose buffer region is on the VAE-decode GPU, the
+    sink pulling each 447,897,600-B frame tensor with its copy-out consume."""
     devs = devices(4, cross)          # stage h runs on devs[h]; hop h's ring sits at its consumer
     cons_dev = [devs[(h + 1) % 4] for h in range(4)]
     nreq, seed = 4, synth.SEED_BASE + 4
     rings, peers, srcs, msgs = [], [], [], []
     for h, (Rb, N, nb) in enumerate(C4_HOPS):
-        rings.append(R.ring_create(cons_dev[h], Rb, N, 1, 0))
+        if h == 3 and frames == "split":
+            rings.append(R.ring_create_split(cons_dev[h], devs[h], Rb, N, 1, 0))
+        else:
+            rings.append(R.ring_create(cons_dev[h], Rb, N, 1, 0))
         pe, mh = R.ring_attach_peer(R.ring_export(rings[h]), devs[h], 0)
         R.ring_bind_mirror(rings[h], 0, mh)
         peers.append(pe)
@@ -263,6 +269,10 @@ def test_c4_stage_chain(R, cross):
     out_args = [[(dev_u64([srcs[h].data_ptr()], dv[h]), dev_u64([C4_HOPS[h][2]], dv[h]),
                   torch.full((1,), h, dtype=torch.int32, device=dv[h]), dev_u64([r], dv[h])) for r in range(nreq)]
                 for h in range(4)]
+    pulled = None
+    if frames == "split":             # the sink's copy-out buffer for one frame tensor
+        pulled = torch.empty(C4_HOPS[3][2], dtype=torch.uint8, device=cv[3])
+        pulled_args = (dev_u64([pulled.data_ptr()], cv[3]), dev_u64([C4_HOPS[3][2]], cv[3]))
     try:
         for r in range(nreq):
             for h in range(5):            # stage h: input hop h-1 (h > 0), output hop h (h < 4)
@@ -270,9 +280,14 @@ def test_c4_stage_chain(R, cross):
                 if h > 0:
                     ring_in = rings[h - 1]
                     v = vt[h - 1][r * 128:(r + 1) * 128]
-                    R.ring_get(ring_in, 1, v, None, 0, 0, s)
-                    bads[h - 1].append(verify_views(ring_in, v, 1, seed, in_ch[h - 1], in_sq[h - 1][r], s))
-                    R.ring_release(ring_in, 1, s)
+                    if h == 4 and pulled is not None:      # pulled over NVLink, then checked in place
+                        R.ring_consume(ring_in, 1, v, pulled, C4_HOPS[3][2], 0, s)
+                        with torch.cuda.device(cons_dev[3]):
+                            bads[3].append(SD.verify(*pulled_args, in_ch[3], in_sq[3][r], seed, s))
+                    else:
+                        R.ring_get(ring_in, 1, v, None, 0, 0, s)
+                        bads[h - 1].append(verify_views(ring_in, v, 1, seed, in_ch[h - 1], in_sq[h - 1][r], s))
+                        R.ring_release(ring_in, 1, s)
                 if h < 4:
                     with torch.cuda.device(devs[h]), torch.cuda.stream(s):
                         SD.fill(*out_args[h][r], seed, s)
