@@ -901,6 +901,11 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   }
   if (lane == 0) {
     st_release<false>(&S->planned, make_planned(L.items, L.units) | kPlannedDone);
+    // A CTA that starts this late (its SM was busy with another kernel) must
+    // not evaluate the first round from the tail written below: it reads the
+    // tail, then this done word (spec_first_round); the fence makes the new
+    // tail imply the done word.
+    fence_acq_rel<false>();
     for (uint32_t d = 0; d < kMaxRouterDests && d < a.n_dests && !L.dead; ++d)
       if (L.loaded & (1u << d)) {
         a.dests[d].st->chan_seq = L.chans[d];
@@ -1212,12 +1217,25 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
     return;
   }
   uint64_t P = 0, H = 0;
+  uint32_t late = 0;
   if (lane == 0) {
     P = __ldcg(reinterpret_cast<const unsigned long long*>(&D.st->tail_cache));
     H = read_head(D);
+    // The tail is this launch's starting tail only while the leader has not
+    // finished: it writes the new tail after its done word (put_leader), so a
+    // CTA dispatched after that -- e.g. its SM was held by another kernel --
+    // sees the done word here and leaves every unit to the leader's plans
+    // (speculating from the new tail would copy into the NEXT launch's entries
+    // and count the unit as done: a unit of this launch never copied).
+    fence_acq_rel<false>();
+    late = planned_done(ld_relaxed<false>(&a.ctx->set[a.launch & 1].planned)) ? 1u : 0u;
   }
   P = __shfl_sync(0xffffffffu, P, 0);
   H = __shfl_sync(0xffffffffu, H, 0);
+  if (__shfl_sync(0xffffffffu, late, 0)) {
+    if (lane == 0) { sp->n_units = 0; sp->n = 0; }
+    return;
+  }
   uint32_t n_msgs = 0, units = 0, items = 0;
   for (int rnd = 0; rnd < kSpecRounds; ++rnd) {
     const uint32_t k0 = rnd * kGroup;
