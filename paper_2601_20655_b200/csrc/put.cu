@@ -901,16 +901,13 @@ __device__ void put_leader(const PutArgs& a, LaunchCtx* ctx, LaunchSet* S) {
   }
   if (lane == 0) {
     st_release<false>(&S->planned, make_planned(L.items, L.units) | kPlannedDone);
-    // A CTA that starts this late (its SM was busy with another kernel) must
-    // not evaluate the first round from the tail written below: it reads the
-    // tail, then this done word (spec_first_round); the fence makes the new
-    // tail imply the done word.
-    fence_acq_rel<false>();
     for (uint32_t d = 0; d < kMaxRouterDests && d < a.n_dests && !L.dead; ++d)
       if (L.loaded & (1u << d)) {
         a.dests[d].st->chan_seq = L.chans[d];
         if (!a.dests[d].mpsc) a.dests[d].st->tail_cache = L.tails[d];
       }
+    // the next launch's starting tail, in ITS counter set (spec_first_round)
+    if (fast && (L.loaded & 1u) && !L.dead) ctx->set[(a.launch + 1) & 1].start_tail = L.tails[0];
   }
   if (lane == 0 && a.engine) {   // the host restarts a closed engine at its next submission
     __threadfence_system();
@@ -1216,23 +1213,24 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
     if (lane == 0) { sp->n_units = 0; sp->n = 0; }
     return;
   }
-  uint64_t P = 0, H = 0;
-  uint32_t late = 0;
+  uint64_t P = 0, H = 0, P0 = 0;
   if (lane == 0) {
     P = __ldcg(reinterpret_cast<const unsigned long long*>(&D.st->tail_cache));
+    // The tail is this launch's starting tail only until the leader finishes
+    // and writes the new one; a CTA dispatched after that -- e.g. its SM was
+    // held by another kernel -- would speculate into the NEXT launch's entries
+    // and count the unit as done (a unit of this launch never copied).  The
+    // previous launch's leader left this launch's starting tail in this
+    // launch's counter set, which no one writes during the launch: speculate
+    // only when the two agree (any other writer of the tail -- a routed
+    // launch, the fused device put -- also makes them differ: no speculation).
+    P0 = __ldcg(reinterpret_cast<const unsigned long long*>(&a.ctx->set[a.launch & 1].start_tail));
     H = read_head(D);
-    // The tail is this launch's starting tail only while the leader has not
-    // finished: it writes the new tail after its done word (put_leader), so a
-    // CTA dispatched after that -- e.g. its SM was held by another kernel --
-    // sees the done word here and leaves every unit to the leader's plans
-    // (speculating from the new tail would copy into the NEXT launch's entries
-    // and count the unit as done: a unit of this launch never copied).
-    fence_acq_rel<false>();
-    late = planned_done(ld_relaxed<false>(&a.ctx->set[a.launch & 1].planned)) ? 1u : 0u;
   }
   P = __shfl_sync(0xffffffffu, P, 0);
+  P0 = __shfl_sync(0xffffffffu, P0, 0);
   H = __shfl_sync(0xffffffffu, H, 0);
-  if (__shfl_sync(0xffffffffu, late, 0)) {
+  if (P != P0) {
     if (lane == 0) { sp->n_units = 0; sp->n = 0; }
     return;
   }

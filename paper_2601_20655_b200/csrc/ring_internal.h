@@ -132,7 +132,10 @@ struct alignas(128) LaunchSet {
   uint32_t _b[31];
   uint32_t next_unit;      // copy work units handed out (atomic)
   uint32_t _c[31];
-  uint32_t _d[32];
+  // the producer-local tail this launch starts from, written by the previous
+  // launch's leader when it finished (put.cu, spec_first_round)
+  uint64_t start_tail;
+  uint32_t _d[30];
   uint32_t arrive[kPlanRing];
 };
 // Bit 31 of the items field: the control warp is done, the word is final.
