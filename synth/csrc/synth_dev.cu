@@ -116,6 +116,23 @@ __global__ void views_to_args(const uint8_t* __restrict__ views, uint32_t n, uin
   }
 }
 
+// Test scaffolding (no payload arithmetic): CTA i occupies its SM -- all of
+// its shared memory, so no other kernel's CTA can start there -- until
+// base_ns + i * step_ns after the kernel started, so SMs become free one at a
+// time (the late-CTA regression test of the ring's put).
+__global__ void hold_sms(uint64_t base_ns, uint64_t step_ns) {
+  extern __shared__ uint8_t hold_smem[];
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (threadIdx.x == 0) hold_smem[0] = 1;
+  const uint64_t until = t0 + base_ns + (uint64_t)blockIdx.x * step_ns;
+  uint64_t t = t0;
+  while (t < until) {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  }
+}
+
 // Kernels are loaded when a device is first used: a lazily loaded module waits
 // for the kernels already running, and the ring tests launch these next to
 // producer / consumer kernels that spin on each other.
@@ -136,6 +153,10 @@ void preload() {
   load(synth_kernel<true>);
   load(init_bad);
   load(views_to_args);
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, hold_sms);
+  cudaFuncSetAttribute(hold_sms, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(hold_sms, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
   done[dev] = true;
 }
 
@@ -194,6 +215,17 @@ int synth_verify_views(const void* d_views, uint32_t n, uint64_t data_base, cons
                                                 d_lut, lut_stride, p, l, c, q);
   if (cudaError_t e = cudaGetLastError()) return (int)e;
   return synth_verify(p, l, c, q, n, seed, d_bad, stream);
+}
+
+// Occupy every SM of the current device (one CTA each, all shared memory),
+// releasing them one at a time: CTA i exits base_ns + i * step_ns after start.
+int synth_hold_sms(uint64_t base_ns, uint64_t step_ns, cudaStream_t stream) {
+  preload();
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  hold_sms<<<nsm, 32, 200 << 10, stream>>>(base_ns, step_ns);
+  return (int)cudaGetLastError();
 }
 
 // Host reference of one word (a check that both sides agree on the formula).

@@ -41,6 +41,8 @@ def lib():
         L.synth_verify.restype = C.c_int
         L.synth_verify_views.argtypes = [P, U32, U64, P, P, P, U64, U64, P, P, P]
         L.synth_verify_views.restype = C.c_int
+        L.synth_hold_sms.argtypes = [U64, U64, P]
+        L.synth_hold_sms.restype = C.c_int
         L.synth_word.argtypes = [U64, U32, U64, U64]
         L.synth_word.restype = U64
         _lib = L
@@ -123,3 +125,11 @@ def verify_views(views, n: int, data_base: int, seed: int, chans=None, seqs=None
 
 def word(seed: int, channel: int, seq: int, i: int) -> int:
     return int(lib().synth_word(seed & (2**64 - 1), channel, seq, i))
+
+
+def hold_sms(base_ns: int, step_ns: int, stream=None):
+    """Test scaffolding: occupy every SM of the current device (all shared
+    memory) and release them one at a time, SM i after base_ns + i * step_ns."""
+    st = lib().synth_hold_sms(base_ns, step_ns, _stream(stream))
+    if st:
+        raise RuntimeError(f"synth_hold_sms: cudaError {st}")

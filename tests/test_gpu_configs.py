@@ -505,3 +505,56 @@ def test_c5b_epoch_flip(R, cross):
                 R.ring_detach(P["pb"])
         R.ring_destroy(ringA)
         R.ring_destroy(ringB)
+
+
+# ---------------------------------------------------------------------------------------
+# Regression: put CTAs dispatched after their leader finished
+# ---------------------------------------------------------------------------------------
+def test_put_ctas_dispatched_after_the_leader(R):
+    """A put launch whose CTAs start one by one, well after its leader CTA has
+    planned the launch and finished: every SM is held by a test kernel that
+    releases them 2 us apart (synth_hold_sms).  The late CTAs must not
+    speculate the first round from the tail the leader has already moved
+    (before the fix they copied their units into the next launch's entries and
+    counted them: units never copied).  Every payload byte of every launch
+    arrives (device verifier); headers and placements are the oracle's."""
+    seed = synth.SEED_BASE + 77
+    L = Layout(256 << 20, 64)
+    rb = R.ring_create(0, L.R, L.N, 1, R.RING_CREATE_LOCAL)
+    pb, mhb = R.ring_attach_peer(R.ring_export(rb), 0, 0)
+    R.ring_bind_mirror(rb, 0, mhb)
+    launches = 6
+    buf_b, ptr_b = device_sources([(0, k, EMB) for k in range(launches)], seed)
+    hd_b = [synth.header_fields(seed, 0, k) for k in range(launches)]
+    msgs_b = _msgs(R, ptr_b, [EMB] * launches, hd_b, 7, 1, "cuda")
+    st_b = [torch.full((1,), 10, dtype=torch.int32, device="cuda") for _ in range(launches)]
+    vt_b = torch.zeros(launches * 128, dtype=torch.uint8, device="cuda")
+    chans = torch.zeros(1, dtype=torch.int32, device="cuda")
+    keys = [dev_u64([k]) for k in range(launches)]
+    s_hold, s_pb, s_cb = (torch.cuda.Stream() for _ in range(3))
+    bads = []
+    try:
+        for k in range(launches):
+            torch.cuda.synchronize()
+            SD.hold_sms(5_000, 2_000, s_hold)                # every SM busy; freed one per 2 us
+            R.ring_put_batch(pb, msgs_b[k * 48:(k + 1) * 48], 1, 0, st_b[k], s_pb)
+            v = vt_b[k * 128:(k + 1) * 128]
+            R.ring_get(rb, 1, v, None, 0, 0, s_cb)
+            bads.append(verify_views(rb, v, 1, seed, chans, keys[k], s_cb))
+            R.ring_release(rb, 1, s_cb)
+        torch.cuda.synchronize()
+        img = spsc_image(L, [EMB] * launches)
+        ents = [e for e in img["entries"] if not e[3]]
+        v = views_host(vt_b)
+        for k in range(launches):
+            assert st_b[k].cpu().tolist() == [0], k
+            assert int(v[k]["status"]) == 0, k
+            assert _place(v[k]) == (ents[k][1], ents[k][2], ents[k][0]), k
+            h = hd_b[k]
+            assert bytes(v[k]["header"])[:56] == encode_header(h[0], h[1], 7, 1, EMB, 0, k, 0, 0, 0)[:56], k
+        for k, b in enumerate(bads):
+            _ok(b, k)
+    finally:
+        torch.cuda.synchronize()
+        R.ring_detach(pb)
+        R.ring_destroy(rb)
