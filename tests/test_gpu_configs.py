@@ -510,7 +510,8 @@ def test_c5b_epoch_flip(R, cross):
 # ---------------------------------------------------------------------------------------
 # Regression: put CTAs dispatched after their leader finished
 # ---------------------------------------------------------------------------------------
-def test_put_ctas_dispatched_after_the_leader(R):
+@pytest.mark.parametrize("copy_mode", [0, 1])
+def test_put_ctas_dispatched_after_the_leader(R, copy_mode):
     """A put launch whose CTAs start one by one, well after its leader CTA has
     planned the launch and finished: every SM is held by a test kernel that
     releases them 2 us apart (synth_hold_sms).  The late CTAs must not
@@ -523,6 +524,7 @@ def test_put_ctas_dispatched_after_the_leader(R):
     rb = R.ring_create(0, L.R, L.N, 1, R.RING_CREATE_LOCAL)
     pb, mhb = R.ring_attach_peer(R.ring_export(rb), 0, 0)
     R.ring_bind_mirror(rb, 0, mhb)
+    R.ring_peer_config(pb, 0, 0, copy_mode)          # LSU copy warps / TMA engines
     launches = 6
     buf_b, ptr_b = device_sources([(0, k, EMB) for k in range(launches)], seed)
     hd_b = [synth.header_fields(seed, 0, k) for k in range(launches)]
