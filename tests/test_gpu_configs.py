@@ -560,3 +560,40 @@ def test_put_ctas_dispatched_after_the_leader(R, copy_mode):
         torch.cuda.synchronize()
         R.ring_detach(pb)
         R.ring_destroy(rb)
+
+
+def test_get_ctas_dispatched_late(R):
+    """The consumer side of the same hazard: a copy-out consume whose CTAs
+    start one by one (every SM held, freed 2 us apart) after its control warp
+    has planned every entry; the copy warps take their units from the plans
+    only, so every payload byte arrives."""
+    seed = synth.SEED_BASE + 78
+    L = Layout(256 << 20, 64)
+    ring = R.ring_create(0, L.R, L.N, 1, R.RING_CREATE_LOCAL)
+    peer, mh = R.ring_attach_peer(R.ring_export(ring), 0, 0)
+    R.ring_bind_mirror(ring, 0, mh)
+    m, launches = 8, 4
+    lens = [EMB if q % 2 == 0 else LAT480 for q in range(m)]
+    buf, ptrs = device_sources([(0, q, lens[q]) for q in range(m)], seed)
+    msgs = _msgs(R, ptrs, lens, [synth.header_fields(seed, 0, q) for q in range(m)], 7, 1, "cuda")
+    st = torch.full((m,), 10, dtype=torch.int32, device="cuda")
+    vt = torch.zeros(m * 128, dtype=torch.uint8, device="cuda")
+    dst = torch.empty(m * EMB, dtype=torch.uint8, device="cuda")
+    dptr = dev_u64([dst.data_ptr() + q * EMB for q in range(m)])
+    dlen, chans, keys = dev_u64(lens), torch.zeros(m, dtype=torch.int32, device="cuda"), dev_u64(list(range(m)))
+    s_hold, s_c = torch.cuda.Stream(), torch.cuda.Stream()
+    try:
+        for k in range(launches):
+            R.ring_put_batch(peer, msgs, m, 0, st)
+            torch.cuda.synchronize()                          # published before the consume starts
+            SD.hold_sms(5_000, 2_000, s_hold)
+            R.ring_consume(ring, m, vt, dst, EMB, 0, s_c)
+            bad = SD.verify(dptr, dlen, chans, keys, seed, s_c)
+            torch.cuda.synchronize()
+            assert st.cpu().tolist() == [0] * m, k
+            assert (views_host(vt)["status"] == 0).all(), k
+            _ok(bad, k)
+    finally:
+        torch.cuda.synchronize()
+        R.ring_detach(peer)
+        R.ring_destroy(ring)
