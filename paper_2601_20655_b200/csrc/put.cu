@@ -1268,7 +1268,7 @@ __device__ void spec_first_round(const PutArgs& a, SpecRound* sp) {
   }
 }
 
-// MODE 0: LSU copy warps; MODE 1: one TMA engine warp per CTA; MODE 2: LSU
+// MODE 0: LSU copy warps; MODE 1: TMA engine warps; MODE 2: LSU
 // copy warps with 32-B accesses (NVLink destinations).  Separate kernels, so
 // one path's registers never change another's copy loop.
 template <int MODE>

@@ -319,7 +319,8 @@ __device__ __forceinline__ void copy_warp(LaunchCtx* ctx, LaunchSet* S, CopyShar
 // `chunk` is a power of two (host-enforced): a shift, not a 64-bit division
 // (the division subroutine cost ~0.3 us per message in the serial leader path).
 // ---------------------------------------------------------------------------
-// TMA copy engine (copy_mode 1): one warp per CTA drives a ring of `stages`
+// TMA copy engine (copy_mode 1): each engine warp (up to kMaxEngineWarps per
+// CTA, put.cu) drives its own ring of `stages`
 // shared-memory buffers of `chunk` bytes with bulk asynchronous copies
 // (cp.async.bulk global -> shared, completion on an mbarrier; then
 // shared -> global, completion by bulk group).  One elected lane issues; the
