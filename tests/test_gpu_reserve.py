@@ -75,14 +75,17 @@ def test_reserve_commit_concurrent_producers(R, cross):
     # ClaimPad, then UnlockFull -> AdvW / RH) while another sender's smaller
     # message went in after it, so the PADs are where the GPU put them:
     # each one fills [end of the previous entry, R) and is needed by a message
-    # of a waiting sender (one of the next max_producers entries does not fit).
+    # of a waiting sender: the next message of one of the producers after it
+    # does not fit in [pos, R) (the others may place many messages first).
     ent = [(int(x["slot_seq"]), int(x["start"]), int(x["footprint"])) for x in v]
+    pids = [h["producer_id"] for h in hs]
     assert [e[2] for e in ent] == [footprint(L, int(x["len"])) for x in v]
     pos = 0
     for q, (sq, st, f) in enumerate(ent):
         if q and sq == seq_next(seq_next(ent[q - 1][0])):   # one PAD slot in between: [pos, R), then 0
             assert pos < L.R and st == 0, (q, pos, st)
-            assert any(e[2] > L.R - pos for e in ent[q:q + 3]), (q, pos)
+            nxt = [next((j for j in range(q, len(ent)) if pids[j] == p), None) for p in set(pids)]
+            assert any(j is not None and ent[j][2] > L.R - pos for j in nxt), (q, pos)
         else:
             assert q == 0 or sq == seq_next(ent[q - 1][0]), (q, sq, ent[q - 1][0])
             assert st == (pos if pos < L.R else 0), (q, st, pos)
